@@ -1,0 +1,201 @@
+/*
+ * lramm_cuda.h -- C ABI of the B200-native LRAMM approximate-GEMM library
+ * (liblramm_cuda.so, sm_100a).  Plain pointers, sizes and a cudaStream_t; no
+ * torch or NumPy types.  Every entry point returns an lramm_status; on failure
+ * lramm_last_error() (thread-local) holds a one-line message.
+ *
+ * Two families of entry points:
+ *
+ *  (1) HOST-pointer entry points  lramm_host_*  -- what the reference's kernel
+ *      plugin FFI binds.  The reference selects its kernel backend at import
+ *      time in `pkg/src/lramm/_kernels/__init__.py:8-39` and calls exactly four
+ *      functions; each host entry point replaces one of them with identical
+ *      argument meaning (row-major C-contiguous NumPy buffers, caller-owned
+ *      outputs) and identical error behaviour (inner-dimension mismatch ->
+ *      LRAMM_ERR_SHAPE, which the binding raises as ValueError("inner dimensions
+ *      differ"), Jacobi non-convergence -> LRAMM_ERR_NONCONVERGENCE ->
+ *      RuntimeError):
+ *        lramm_host_matmul            <- _core.matmul            (_core.pyx:17-32, _pure.py:10-14)
+ *        lramm_host_imatmul           <- _core.imatmul           (_core.pyx:35-50, _pure.py:17-21)
+ *        lramm_host_scale_round_clip  <- _core.scale_round_clip  (_core.pyx:53-69, _pure.py:24-26)
+ *        lramm_host_svd               <- _jacobi.jacobi_svd      (_jacobi.py:14-50, _pure.py:29-35)
+ *      plus the whole pipeline, which replaces `lramm.pipeline.lramm`
+ *      (pipeline.py:159-214) in one call:
+ *        lramm_host_lramm
+ *      Host entry points copy host->device, compute, copy device->host and
+ *      synchronise; they manage their own (cached) device memory.
+ *
+ *  (2) DEVICE-pointer entry points  lramm_*  -- stream-ordered, caller-allocated
+ *      device buffers and workspace, no host synchronisation and no allocation,
+ *      CUDA-graph capturable.  Used by the Python package with torch tensors.
+ *
+ * Status codes map 1:1 onto the reference's exception types (errors.py:4-33):
+ * SHAPE -> ShapeError, PARAM -> ParameterError, OVERFLOW -> OverflowRiskError,
+ * NONFINITE -> ParameterError("cannot quantize non-finite entries", quant.py:63-64),
+ * NONCONVERGENCE -> RuntimeError (_jacobi.py:31-32), UNSUPPORTED -> NotImplementedError
+ * (e.g. bit budgets above 8 on the int8 tensor-core path), CUDA -> RuntimeError.
+ */
+#ifndef LRAMM_CUDA_H_
+#define LRAMM_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *lramm_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  LRAMM_OK = 0,
+  LRAMM_ERR_SHAPE = 1,
+  LRAMM_ERR_PARAM = 2,
+  LRAMM_ERR_OVERFLOW = 3,
+  LRAMM_ERR_NONCONVERGENCE = 4,
+  LRAMM_ERR_UNSUPPORTED = 5,
+  LRAMM_ERR_CUDA = 6,
+  LRAMM_ERR_NONFINITE = 7,
+  LRAMM_ERR_WORKSPACE = 8
+} lramm_status;
+
+typedef enum { LRAMM_F32 = 0, LRAMM_F64 = 1, LRAMM_I8 = 2, LRAMM_I32 = 3, LRAMM_I64 = 4, LRAMM_I4 = 5 } lramm_dtype;
+typedef enum { LRAMM_GRAN_TENSOR = 0, LRAMM_GRAN_ROW = 1, LRAMM_GRAN_COL = 2 } lramm_granularity;
+typedef enum { LRAMM_MODE_PARITY = 0, LRAMM_MODE_FAST = 1 } lramm_mode;
+
+/* Pipeline parameters: mirrors LrammParams (pipeline.py:50-70) plus the fast-mode
+ * extension (SURVEY §7 "Params").  sketch/power/proj bits of 0 mean fp64 (the
+ * reference's behaviour, rsvd.py:57-64,77). */
+typedef struct {
+  int32_t rank;
+  int32_t oversample;
+  int32_t power_iters;
+  int32_t bits[3]; /* (d1, d2, d3), each in [2, 8] on device */
+  double alpha;
+  double beta;
+  int32_t mode;        /* lramm_mode */
+  int32_t sketch_bits; /* Y = X.Omega              (fast mode) */
+  int32_t power_bits;  /* X^T.Q and X.Qz           (fast mode) */
+  int32_t proj_bits;   /* Q^T.X                    (fast mode) */
+  int32_t granularity; /* lramm_granularity of the sketch products */
+  int32_t reserved;
+} lramm_params_t;
+
+/* Per-stage device time in milliseconds, keys of pipeline.STAGES (pipeline.py:37). */
+typedef struct {
+  float rsvd_ms, scaling_ms, gemm1_ms, gemm2_ms, gemm3_ms;
+} lramm_timings_t;
+
+/* Integer-GEMM epilogue: out = alpha * (acc / (row_scale[i] * col_scale[j])) + beta * C
+ * (quant.py:116-121 dequantisation, bit-exact in fp64), or raw int32 (optionally
+ * accumulated with atomics for split-K; exact and order independent). */
+typedef struct {
+  int32_t out_dtype;     /* LRAMM_I32, LRAMM_F32 or LRAMM_F64 */
+  int32_t accumulate;    /* LRAMM_I32 only: out += acc (out pre-zeroed) */
+  int32_t transpose_out; /* store out^T (N x M, leading dim ldo) */
+  int32_t c_dtype;       /* LRAMM_F32 / LRAMM_F64 when c != NULL */
+  void *out;
+  int64_t ldo;
+  const double *row_scale; /* NULL => 1.0 */
+  int64_t row_scale_inc;   /* 0 => per-tensor (broadcast element 0) */
+  const double *col_scale;
+  int64_t col_scale_inc;
+  double alpha;
+  double beta;
+  const void *c;
+  int64_t ldc;
+} lramm_epilogue_t;
+
+const char *lramm_last_error(void);
+const char *lramm_version(void);
+/* 0 if a compute-capability 10.0 device is current, else LRAMM_ERR_UNSUPPORTED. */
+int lramm_device_check(void);
+
+/* ---------------------------------------------------------------- device API */
+
+/* Symmetric absmax quantiser (quant.py:55-71) at granularity tensor / row / col.
+ * x: rows x cols (leading dim ldx, elements) of dtype LRAMM_F32 or LRAMM_F64.
+ * q_dtype LRAMM_I8: int8 output, LRAMM_I32: int32 output (the reference's
+ * container), LRAMM_I4: two's-complement nibbles packed along each output row
+ * (low nibble = even column), bits <= 4.  transpose_out writes q^T.  Padding
+ * columns of q up to ldq are zeroed.  scales: 1 (tensor), rows or cols doubles,
+ * scale = cap / amax (all-zero -> 1.0).  nonfinite_flag (device int, may be NULL)
+ * is set to 1 if x holds a non-finite value.  ws >= lramm_quantize_ws(rows, cols). */
+int lramm_quantize(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits,
+                   int granularity, int transpose_out, void *q, int q_dtype, int64_t ldq,
+                   double *scales, int *nonfinite_flag, void *ws, size_t ws_bytes,
+                   lramm_stream_t stream);
+size_t lramm_quantize_ws(int64_t rows, int64_t cols);
+
+/* rint(a*scale) half-to-even, clamp +-cap, int32 (the plugin kernel, _core.pyx:53-69). */
+int lramm_scale_round_clip(const double *a, int64_t rows, int64_t cols, int64_t lda, double scale,
+                           int cap, int32_t *out, int64_t ldo, lramm_stream_t stream);
+
+/* C = A . B^T with A: M x K int8 (row-major, lda bytes), B: N x K int8 (row-major,
+ * ldb bytes), int32 accumulation in tensor memory (tcgen05.mma kind::i8, TMA-fed).
+ * lda, ldb must be multiples of 16; A/B 16-byte aligned.  split_k > 1 requires an
+ * int32 output with accumulate = 1. */
+int lramm_igemm(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, const int8_t *b,
+                int64_t ldb, const lramm_epilogue_t *epi, int split_k, lramm_stream_t stream);
+
+/* fp64 GEMM.  trans_a = 0: C(MxN) = A(MxK) . B(KxN); trans_a = 1: C = A^T . B with
+ * A stored K x M (split-K over the long dimension, deterministic reduction).
+ * All row-major.  ws >= lramm_dgemm_ws(trans_a, M, N, K). */
+int lramm_dgemm(int trans_a, int64_t M, int64_t N, int64_t K, const double *a, int64_t lda,
+                const double *b, int64_t ldb, double *c, int64_t ldc, void *ws, size_t ws_bytes,
+                lramm_stream_t stream);
+size_t lramm_dgemm_ws(int trans_a, int64_t M, int64_t N, int64_t K);
+
+/* Thin QR of a tall m x w fp64 matrix (m >= w): CholeskyQR2 with an on-device
+ * Householder fallback when the Gram matrix is not numerically positive definite.
+ * q (m x w, may alias y) and r (w x w upper) are outputs; r may be NULL. */
+int lramm_qr(const double *y, int64_t m, int64_t w, int64_t ldy, double *q, int64_t ldq, double *r,
+             void *ws, size_t ws_bytes, lramm_stream_t stream);
+size_t lramm_qr_ws(int64_t m, int64_t w);
+
+/* Thin SVD of a dense fp64 m x n matrix (the reference's oracle_svd contract,
+ * matcore.py:232-245): u m x t, s t (descending), v n x t, t = min(m, n).
+ * Implementation: CholeskyQR2 reduction + one-sided Jacobi (tol 1e-13,
+ * <= 60 sweeps, _jacobi.py:10-11) on device; info (device int) receives the
+ * sweep count or -1 on non-convergence. */
+int lramm_svd(const double *a, int64_t m, int64_t n, double *u, double *s, double *v, int *info,
+              void *ws, size_t ws_bytes, lramm_stream_t stream);
+size_t lramm_svd_ws(int64_t m, int64_t n);
+
+/* Randomised SVD of x (rows x cols, F32 or F64) truncated to params->rank
+ * (rsvd.py:68-94): u rows x rank, s rank, v cols x rank.  omega: cols x w fp64,
+ * w = min(rank + oversample, min(rows, cols)), drawn by the caller exactly as
+ * rsvd.py:56 (NumPy Philox).  status (device int): 0 ok, else an lramm_status. */
+int lramm_rsvd(const void *x, int x_dtype, int64_t rows, int64_t cols, const lramm_params_t *params,
+               const double *omega, double *u, double *s, double *v, int *status, void *ws,
+               size_t ws_bytes, lramm_stream_t stream);
+size_t lramm_rsvd_ws(int64_t rows, int64_t cols, const lramm_params_t *params);
+
+/* The whole pipeline (pipeline.py:159-214): d = alpha * QM(QM(QM(Va^T Ub) Zsc) ... ) + beta * c.
+ * a: m x k, b: k x n (F32 or F64, row-major, contiguous).  d: m x n of d_dtype
+ * (LRAMM_F64 reproduces the reference's float64 output bit-for-bit given the same
+ * factors; LRAMM_F32 is its correct rounding).  status: device int (0 = ok).
+ * timings may be NULL; if not NULL the call records events and synchronises the
+ * stream at the end to fill it. */
+int lramm_lramm(const void *a, const void *b, int in_dtype, int64_t m, int64_t k, int64_t n,
+                const lramm_params_t *params, const double *omega_a, const double *omega_b,
+                const void *c, int c_dtype, void *d, int d_dtype, int *status, void *ws,
+                size_t ws_bytes, lramm_timings_t *timings, lramm_stream_t stream);
+size_t lramm_lramm_ws(int64_t m, int64_t k, int64_t n, const lramm_params_t *params);
+
+/* ---------------------------------------------------------------- host API */
+
+int lramm_host_matmul(const double *a, const double *b, double *out, int64_t m, int64_t k, int64_t n);
+int lramm_host_imatmul(const int32_t *a, const int32_t *b, int64_t *out, int64_t m, int64_t k,
+                       int64_t n);
+int lramm_host_scale_round_clip(const double *a, int64_t m, int64_t n, double scale, int cap,
+                                int32_t *out);
+int lramm_host_svd(const double *a, int64_t m, int64_t n, double *u, double *s, double *v);
+int lramm_host_lramm(const void *a, const void *b, int in_dtype, int64_t m, int64_t k, int64_t n,
+                     const lramm_params_t *params, const double *omega_a, const double *omega_b,
+                     const void *c, int c_dtype, void *d, int d_dtype, lramm_timings_t *timings);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LRAMM_CUDA_H_ */

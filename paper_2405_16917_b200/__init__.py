@@ -1,0 +1,50 @@
+"""B200-native LRAMM approximate matrix multiply (arXiv 2405.16917, Algorithm 3).
+
+Drop-in for the hot path of the reference package `lramm`
+(`pkg/src/lramm/__init__.py:6-76`): the same names for the pipeline, the
+randomised SVD, the quantiser and quantised GEMM, the parameter/timing
+dataclasses and the error types, computed by hand-written sm_100a CUDA
+(liblramm_cuda.so, C ABI in include/lramm_cuda.h).  Out of scope:
+bound evaluators, CLI, file I/O, input generators, evaluate/report.
+"""
+
+from . import _native  # noqa: F401  (fails loudly if liblramm_cuda.so is missing)
+from .errors import (
+    DegenerateDenominatorError,
+    LrammError,
+    OracleLimitError,
+    OverflowRiskError,
+    ParameterError,
+    ShapeError,
+    UnsupportedError,
+)
+from .kernels import backend_name
+from .pipeline import (
+    STAGES,
+    CostModel,
+    LrammParams,
+    StageTimings,
+    cost_model,
+    gemm,
+    lramm,
+    lramm_device,
+    preset,
+)
+from .quant import (
+    QuantizedMatrix,
+    bit_cap,
+    dequantize,
+    integer_matmul,
+    qgemm,
+    quantize,
+)
+from .rsvd import (
+    RsvdParams,
+    SvdFactors,
+    oracle_svd,
+    range_finder,
+    rsvd,
+    truncate_svd,
+)
+
+__version__ = "0.1.0"

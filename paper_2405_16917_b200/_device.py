@@ -1,0 +1,116 @@
+"""Device plumbing: torch owns device memory and streams; the compute is liblramm_cuda."""
+
+from __future__ import annotations
+
+import ctypes
+from collections import OrderedDict
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ShapeError
+
+_checked: set[int] = set()
+
+
+def require_device(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("liblramm_cuda needs a CUDA device (sm_100a); there is no CPU fallback")
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index)
+    if dev.index not in _checked:
+        with torch.cuda.device(dev):
+            N.check(N.LIB.lramm_device_check())
+        _checked.add(dev.index)
+    return dev
+
+
+def stream_handle(device=None) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def ptr(t) -> ctypes.c_void_p:
+    if t is None:
+        return ctypes.c_void_p(0)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class _Workspace:
+    """Grow-only scratch per (device, stream); stream ordering makes reuse safe."""
+
+    def __init__(self):
+        self.bufs: dict[tuple[int, int], torch.Tensor] = {}
+
+    def get(self, nbytes: int, device: torch.device) -> torch.Tensor:
+        key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+        buf = self.bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            if buf is not None:
+                del self.bufs[key]
+                del buf
+            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+            self.bufs[key] = buf
+        return buf
+
+
+WORKSPACE = _Workspace()
+
+
+def dtype_code(t) -> int:
+    if t.dtype in (torch.float32, np.float32):
+        return N.F32
+    if t.dtype in (torch.float64, np.float64):
+        return N.F64
+    raise ShapeError(f"unsupported dtype {t.dtype}")
+
+
+def to_device_matrix(a, device: torch.device, keep_f32: bool = True) -> torch.Tensor:
+    """2-D contiguous float32/float64 device tensor (float32 kept: it upcasts exactly on device)."""
+    if isinstance(a, torch.Tensor):
+        t = a
+        if t.dtype not in (torch.float32, torch.float64) or (t.dtype == torch.float32 and not keep_f32):
+            t = t.to(torch.float64)
+        return t.to(device).contiguous()
+    arr = np.asarray(a)
+    if arr.dtype != np.float32 or not keep_f32:
+        arr = np.asarray(arr, dtype=np.float64)
+    return torch.from_numpy(np.ascontiguousarray(arr)).to(device)
+
+
+class OmegaCache:
+    """Gaussian test matrices drawn exactly as the reference (rsvd.py:56, matcore.py:89-92),
+    cached per (seed, ncols, width) on the host and per device."""
+
+    def __init__(self, capacity: int = 16):
+        self.capacity = capacity
+        self.host: OrderedDict = OrderedDict()
+        self.dev: OrderedDict = OrderedDict()
+
+    def host_omega(self, seed: int, ncols: int, width: int) -> np.ndarray:
+        key = (int(seed), int(ncols), int(width))
+        om = self.host.get(key)
+        if om is None:
+            entropy = [int(seed) & 0xFFFFFFFFFFFFFFFF, 0x534B, int(ncols), int(width)]
+            g = np.random.Generator(np.random.Philox(np.random.SeedSequence(entropy)))
+            om = np.ascontiguousarray(g.standard_normal((ncols, width)))
+            self.host[key] = om
+            if len(self.host) > self.capacity:
+                self.host.popitem(last=False)
+        else:
+            self.host.move_to_end(key)
+        return om
+
+    def device_omega(self, seed: int, ncols: int, width: int, device: torch.device) -> torch.Tensor:
+        key = (int(seed), int(ncols), int(width), device.index)
+        t = self.dev.get(key)
+        if t is None:
+            t = torch.from_numpy(self.host_omega(seed, ncols, width)).to(device)
+            self.dev[key] = t
+            if len(self.dev) > self.capacity:
+                self.dev.popitem(last=False)
+        else:
+            self.dev.move_to_end(key)
+        return t
+
+
+OMEGA = OmegaCache()

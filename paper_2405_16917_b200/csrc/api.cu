@@ -1,0 +1,371 @@
+// extern "C" entry points of liblramm_cuda.so (include/lramm_cuda.h).
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace lramm {
+
+static thread_local std::string g_err;
+
+void set_error(const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+int fail(int code, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
+// internal entry points
+int quantize_device(const void *, int, int64_t, int64_t, int64_t, int, int, int, void *, int, int64_t, double *, int *,
+                    void *, size_t, cudaStream_t);
+size_t quantize_ws_bytes(int64_t, int64_t);
+int scale_round_clip_device(const double *, int64_t, int64_t, int64_t, double, int, int32_t *, int64_t, cudaStream_t);
+int igemm_device(int64_t, int64_t, int64_t, const int8_t *, int64_t, const int8_t *, int64_t, const lramm_epilogue_t &,
+                 int, cudaStream_t);
+int dgemm_device(int, int64_t, int64_t, int64_t, const double *, int64_t, const double *, int64_t, double *, int64_t,
+                 void *, size_t, cudaStream_t);
+size_t dgemm_ws_bytes(int, int64_t, int64_t, int64_t);
+int qr_device(const double *, int64_t, int64_t, int64_t, double *, int64_t, double *, void *, size_t, cudaStream_t);
+size_t qr_ws_bytes(int64_t, int64_t);
+int svd_tall_device(const double *, int64_t, int64_t, int64_t, double *, int64_t, double *, double *, int64_t, int *,
+                    int *, void *, size_t, cudaStream_t);
+size_t svd_tall_ws_bytes(int64_t, int64_t);
+int transpose_device(const double *, int64_t, int64_t, int64_t, double *, int64_t, cudaStream_t);
+size_t rsvd_ws_bytes(int64_t, int64_t, const lramm_params_t &, int);
+int rsvd_device(const void *, int, int64_t, int64_t, const lramm_params_t &, const double *, double *, double *,
+                double *, int *, void *, size_t, cudaStream_t);
+size_t lramm_ws_bytes(int64_t, int64_t, int64_t, const lramm_params_t &, int);
+int lramm_device(const void *, const void *, int, int64_t, int64_t, int64_t, const lramm_params_t &, const double *,
+                 const double *, const void *, int, void *, int, int *, void *, size_t, lramm_timings_t *,
+                 cudaStream_t);
+
+// ---------------------------------------------------------------- host-side device memory
+// One cached device arena + stream for the host-pointer entry points (grow-only,
+// serialised by a mutex; the device-pointer API never allocates).
+struct HostCtx {
+  std::mutex mu;
+  char *buf = nullptr;
+  size_t cap = 0;
+  cudaStream_t st = nullptr;
+  int *status = nullptr;
+  int dev = -1;
+};
+static HostCtx &host_ctx() {
+  static HostCtx c;
+  return c;
+}
+static int host_reserve(HostCtx &c, size_t bytes) {
+  int dev = 0;
+  LRAMM_CUDA_TRY(cudaGetDevice(&dev));
+  if (c.dev != dev) {  // new device: drop the old cache
+    c.buf = nullptr;
+    c.cap = 0;
+    c.st = nullptr;
+    c.status = nullptr;
+    c.dev = dev;
+  }
+  if (!c.st) LRAMM_CUDA_TRY(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
+  if (!c.status) LRAMM_CUDA_TRY(cudaMalloc(&c.status, 64));
+  if (bytes > c.cap) {
+    if (c.buf) LRAMM_CUDA_TRY(cudaFree(c.buf));
+    c.buf = nullptr;
+    size_t want = round_up((int64_t)bytes, 1 << 20);
+    LRAMM_CUDA_TRY(cudaMalloc(&c.buf, want));
+    c.cap = want;
+  }
+  return LRAMM_OK;
+}
+
+}  // namespace lramm
+
+using namespace lramm;
+
+extern "C" {
+
+const char *lramm_last_error(void) { return g_err.c_str(); }
+const char *lramm_version(void) { return "lramm-b200 0.1.0 (sm_100a)"; }
+
+int lramm_device_check(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(LRAMM_ERR_UNSUPPORTED, "no CUDA device");
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0)
+    return fail(LRAMM_ERR_UNSUPPORTED, "liblramm_cuda is built for sm_100a; device is sm_%d%d", major, minor);
+  return LRAMM_OK;
+}
+
+int lramm_quantize(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits, int granularity,
+                   int transpose_out, void *q, int q_dtype, int64_t ldq, double *scales, int *nonfinite_flag, void *ws,
+                   size_t ws_bytes, lramm_stream_t stream) {
+  return quantize_device(x, x_dtype, rows, cols, ldx, bits, granularity, transpose_out, q, q_dtype, ldq, scales,
+                         nonfinite_flag, ws, ws_bytes, (cudaStream_t)stream);
+}
+size_t lramm_quantize_ws(int64_t rows, int64_t cols) { return quantize_ws_bytes(rows, cols); }
+
+int lramm_scale_round_clip(const double *a, int64_t rows, int64_t cols, int64_t lda, double scale, int cap, int32_t *out,
+                           int64_t ldo, lramm_stream_t stream) {
+  return scale_round_clip_device(a, rows, cols, lda, scale, cap, out, ldo, (cudaStream_t)stream);
+}
+
+int lramm_igemm(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, const int8_t *b, int64_t ldb,
+                const lramm_epilogue_t *epi, int split_k, lramm_stream_t stream) {
+  if (!epi) return fail(LRAMM_ERR_PARAM, "igemm: epilogue is NULL");
+  return igemm_device(M, N, K, a, lda, b, ldb, *epi, split_k, (cudaStream_t)stream);
+}
+
+int lramm_dgemm(int trans_a, int64_t M, int64_t N, int64_t K, const double *a, int64_t lda, const double *b,
+                int64_t ldb, double *c, int64_t ldc, void *ws, size_t ws_bytes, lramm_stream_t stream) {
+  return dgemm_device(trans_a, M, N, K, a, lda, b, ldb, c, ldc, ws, ws_bytes, (cudaStream_t)stream);
+}
+size_t lramm_dgemm_ws(int trans_a, int64_t M, int64_t N, int64_t K) { return dgemm_ws_bytes(trans_a, M, N, K); }
+
+int lramm_qr(const double *y, int64_t m, int64_t w, int64_t ldy, double *q, int64_t ldq, double *r, void *ws,
+             size_t ws_bytes, lramm_stream_t stream) {
+  return qr_device(y, m, w, ldy, q, ldq, r, ws, ws_bytes, (cudaStream_t)stream);
+}
+size_t lramm_qr_ws(int64_t m, int64_t w) { return qr_ws_bytes(m, w); }
+
+// SVD (matcore.oracle_svd contract).  Tall: u = A H S^-1, v = H.  Wide: work on A^T.
+size_t lramm_svd_ws(int64_t m, int64_t n) {
+  int64_t t = std::min(m, n), l = std::max(m, n);
+  return svd_tall_ws_bytes(l, t) + (size_t)round_up(l * t * 8, 256) + 512;
+}
+int lramm_svd(const double *a, int64_t m, int64_t n, double *u, double *s, double *v, int *info, void *ws,
+              size_t ws_bytes, lramm_stream_t stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m < 1 || n < 1) return fail(LRAMM_ERR_SHAPE, "svd: empty matrix");
+  const int64_t t = std::min(m, n), l = std::max(m, n);
+  if (ws_bytes < lramm_svd_ws(m, n)) return fail(LRAMM_ERR_WORKSPACE, "svd: workspace too small");
+  Arena ar(ws, ws_bytes);
+  double *at = ar.take<double>(l * t);
+  int *st_compl = ar.take<int>(4);
+  size_t rest = ws_bytes - ar.off;
+  void *inner = (char *)ws + ar.off;
+  LRAMM_CUDA_TRY(cudaMemsetAsync(st_compl, 0, 16, st));
+  if (m >= n)
+    return svd_tall_device(a, m, n, n, u, n, s, v, n, info, st_compl, inner, rest, st);
+  // wide: A^T (n x m) = P S H^T  =>  A = H S P^T : u = H, v = P
+  LRAMM_TRY(transpose_device(a, m, n, n, at, m, st));
+  return svd_tall_device(at, n, m, m, v, m, s, u, m, info, st_compl, inner, rest, st);
+}
+
+size_t lramm_rsvd_ws(int64_t rows, int64_t cols, const lramm_params_t *params) {
+  return params ? rsvd_ws_bytes(rows, cols, *params, LRAMM_F32) : 0;
+}
+int lramm_rsvd(const void *x, int x_dtype, int64_t rows, int64_t cols, const lramm_params_t *params,
+               const double *omega, double *u, double *s, double *v, int *status, void *ws, size_t ws_bytes,
+               lramm_stream_t stream) {
+  if (!params) return fail(LRAMM_ERR_PARAM, "rsvd: params is NULL");
+  return rsvd_device(x, x_dtype, rows, cols, *params, omega, u, s, v, status, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t lramm_lramm_ws(int64_t m, int64_t k, int64_t n, const lramm_params_t *params) {
+  return params ? lramm_ws_bytes(m, k, n, *params, LRAMM_F32) : 0;
+}
+int lramm_lramm(const void *a, const void *b, int in_dtype, int64_t m, int64_t k, int64_t n,
+                const lramm_params_t *params, const double *omega_a, const double *omega_b, const void *c, int c_dtype,
+                void *d, int d_dtype, int *status, void *ws, size_t ws_bytes, lramm_timings_t *timings,
+                lramm_stream_t stream) {
+  if (!params) return fail(LRAMM_ERR_PARAM, "lramm: params is NULL");
+  return lramm_device(a, b, in_dtype, m, k, n, *params, omega_a, omega_b, c, c_dtype, d, d_dtype, status, ws, ws_bytes,
+                      timings, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------- host API
+static int finish(HostCtx &c) {
+  LRAMM_CUDA_TRY(cudaStreamSynchronize(c.st));
+  int s = 0;
+  LRAMM_CUDA_TRY(cudaMemcpy(&s, c.status, sizeof(int), cudaMemcpyDeviceToHost));
+  if (s == LRAMM_ERR_NONCONVERGENCE) return fail(s, "jacobi sweeps did not converge within 60");
+  if (s == LRAMM_ERR_NONFINITE) return fail(s, "cannot quantize non-finite entries");
+  if (s) return fail(s, "device status %d", s);
+  return LRAMM_OK;
+}
+
+int lramm_host_matmul(const double *a, const double *b, double *out, int64_t m, int64_t k, int64_t n) {
+  if (m < 1 || k < 1 || n < 1) return fail(LRAMM_ERR_SHAPE, "inner dimensions differ");
+  HostCtx &c = host_ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  size_t gw = dgemm_ws_bytes(0, m, n, k);
+  size_t need = (size_t)round_up((m * k + k * n + m * n) * 8, 256) * 1 + gw + 4096;
+  LRAMM_TRY(host_reserve(c, need));
+  Arena ar(c.buf, c.cap);
+  double *da = ar.take<double>(m * k), *db = ar.take<double>(k * n), *dc = ar.take<double>(m * n);
+  void *w = ar.take<char>((int64_t)gw + 8);
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(da, a, m * k * 8, cudaMemcpyHostToDevice, c.st));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(db, b, k * n * 8, cudaMemcpyHostToDevice, c.st));
+  LRAMM_TRY(dgemm_device(0, m, n, k, da, k, db, n, dc, n, w, gw, c.st));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(out, dc, m * n * 8, cudaMemcpyDeviceToHost, c.st));
+  LRAMM_CUDA_TRY(cudaMemsetAsync(c.status, 0, 4, c.st));
+  return finish(c);
+}
+
+namespace {
+__global__ void i32_to_i8_kernel(const int32_t *__restrict__ x, int64_t rows, int64_t cols, int transpose,
+                                 int8_t *__restrict__ y, int64_t ldy, int *bad) {
+  int64_t n = rows * cols;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / cols, c = i - r * cols;
+    int v = x[i];
+    if (v < -127 || v > 127) *bad = 1;
+    if (transpose)
+      y[c * ldy + r] = (int8_t)v;
+    else
+      y[r * ldy + c] = (int8_t)v;
+  }
+}
+__global__ void i32_to_i64_kernel(const int32_t *__restrict__ x, int64_t n, int64_t *__restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = x[i];
+}
+__global__ void max_abs_i32_kernel(const int32_t *x, int64_t n, unsigned *out) {
+  unsigned m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int v = x[i];
+    unsigned a = v < 0 ? (unsigned)(-(int64_t)v) : (unsigned)v;
+    m = a > m ? a : m;
+  }
+  atomicMax(out, m);
+}
+}  // namespace
+
+// exact int32 x int32 -> int64 for |entries| <= 127 (bit budgets <= 8) on the int8 tensor cores
+int lramm_host_imatmul(const int32_t *a, const int32_t *b, int64_t *out, int64_t m, int64_t k, int64_t n) {
+  if (m < 1 || k < 1 || n < 1) return fail(LRAMM_ERR_SHAPE, "inner dimensions differ");
+  HostCtx &c = host_ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  const int64_t ldk = round_up(k, 16);
+  size_t need = (size_t)round_up((m * k + k * n) * 4, 256) + round_up((m + n) * ldk, 256) + round_up(m * n * 4, 256) +
+                round_up(m * n * 8, 256) + 8192;
+  LRAMM_TRY(host_reserve(c, need));
+  Arena ar(c.buf, c.cap);
+  int32_t *da = ar.take<int32_t>(m * k), *db = ar.take<int32_t>(k * n);
+  int8_t *qa = ar.take<int8_t>(m * ldk), *qb = ar.take<int8_t>(n * ldk);
+  int32_t *acc = ar.take<int32_t>(m * n);
+  int64_t *o64 = ar.take<int64_t>(m * n);
+  int *bad = ar.take<int>(4);
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(da, a, m * k * 4, cudaMemcpyHostToDevice, c.st));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(db, b, k * n * 4, cudaMemcpyHostToDevice, c.st));
+  LRAMM_CUDA_TRY(cudaMemsetAsync(bad, 0, 16, c.st));
+  LRAMM_CUDA_TRY(cudaMemsetAsync(qa, 0, m * ldk, c.st));
+  LRAMM_CUDA_TRY(cudaMemsetAsync(qb, 0, n * ldk, c.st));
+  int grid = 4 * num_sms();
+  i32_to_i8_kernel<<<grid, 256, 0, c.st>>>(da, m, k, 0, qa, ldk, bad);
+  i32_to_i8_kernel<<<grid, 256, 0, c.st>>>(db, k, n, 1, qb, ldk, bad);  // B^T: n x k
+  LRAMM_LAUNCH_CHECK();
+  int hbad = 0;
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, c.st));
+  LRAMM_CUDA_TRY(cudaStreamSynchronize(c.st));
+  if (hbad) return fail(LRAMM_ERR_UNSUPPORTED, "imatmul: entries beyond +-127 need the multi-limb path");
+  if ((double)k * 127.0 * 127.0 >= 2147483648.0) return fail(LRAMM_ERR_OVERFLOW, "imatmul: k too large for int32");
+  lramm_epilogue_t e = {};
+  e.out_dtype = LRAMM_I32;
+  e.out = acc;
+  e.ldo = n;
+  LRAMM_TRY(igemm_device(m, n, k, qa, ldk, qb, ldk, e, 1, c.st));
+  i32_to_i64_kernel<<<grid, 256, 0, c.st>>>(acc, m * n, o64);
+  LRAMM_LAUNCH_CHECK();
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(out, o64, m * n * 8, cudaMemcpyDeviceToHost, c.st));
+  LRAMM_CUDA_TRY(cudaMemsetAsync(c.status, 0, 4, c.st));
+  return finish(c);
+}
+
+int lramm_host_scale_round_clip(const double *a, int64_t m, int64_t n, double scale, int cap, int32_t *out) {
+  if (m < 1 || n < 1) return fail(LRAMM_ERR_SHAPE, "empty matrix");
+  HostCtx &c = host_ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  LRAMM_TRY(host_reserve(c, (size_t)round_up(m * n * 8, 256) + round_up(m * n * 4, 256) + 4096));
+  Arena ar(c.buf, c.cap);
+  double *da = ar.take<double>(m * n);
+  int32_t *dq = ar.take<int32_t>(m * n);
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(da, a, m * n * 8, cudaMemcpyHostToDevice, c.st));
+  LRAMM_TRY(scale_round_clip_device(da, m, n, n, scale, cap, dq, n, c.st));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(out, dq, m * n * 4, cudaMemcpyDeviceToHost, c.st));
+  LRAMM_CUDA_TRY(cudaMemsetAsync(c.status, 0, 4, c.st));
+  return finish(c);
+}
+
+int lramm_host_svd(const double *a, int64_t m, int64_t n, double *u, double *s, double *v) {
+  if (m < 1 || n < 1) return fail(LRAMM_ERR_SHAPE, "empty matrix");
+  HostCtx &c = host_ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  const int64_t t = std::min(m, n);
+  size_t ws = lramm_svd_ws(m, n);
+  LRAMM_TRY(host_reserve(c, (size_t)round_up((m * n + m * t + t + n * t) * 8, 256) + ws + 8192));
+  Arena ar(c.buf, c.cap);
+  double *da = ar.take<double>(m * n), *du = ar.take<double>(m * t), *ds = ar.take<double>(t),
+         *dv = ar.take<double>(n * t);
+  void *w = ar.take<char>((int64_t)ws);
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(da, a, m * n * 8, cudaMemcpyHostToDevice, c.st));
+  LRAMM_CUDA_TRY(cudaMemsetAsync(c.status, 0, 16, c.st));
+  LRAMM_TRY(lramm_svd(da, m, n, du, ds, dv, c.status + 1, w, ws, (lramm_stream_t)c.st));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(u, du, m * t * 8, cudaMemcpyDeviceToHost, c.st));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(s, ds, t * 8, cudaMemcpyDeviceToHost, c.st));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(v, dv, n * t * 8, cudaMemcpyDeviceToHost, c.st));
+  LRAMM_CUDA_TRY(cudaStreamSynchronize(c.st));
+  int info = 0;
+  LRAMM_CUDA_TRY(cudaMemcpy(&info, c.status + 1, sizeof(int), cudaMemcpyDeviceToHost));
+  if (info < 0) return fail(LRAMM_ERR_NONCONVERGENCE, "jacobi sweeps did not converge within 60");
+  return LRAMM_OK;
+}
+
+int lramm_host_lramm(const void *a, const void *b, int in_dtype, int64_t m, int64_t k, int64_t n,
+                     const lramm_params_t *params, const double *omega_a, const double *omega_b, const void *cmat,
+                     int c_dtype, void *d, int d_dtype, lramm_timings_t *timings) {
+  if (!params) return fail(LRAMM_ERR_PARAM, "lramm: params is NULL");
+  if (in_dtype != LRAMM_F32 && in_dtype != LRAMM_F64) return fail(LRAMM_ERR_PARAM, "inputs must be F32 or F64");
+  HostCtx &c = host_ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  const int64_t es = in_dtype == LRAMM_F32 ? 4 : 8, ds = d_dtype == LRAMM_F32 ? 4 : 8,
+                cs = c_dtype == LRAMM_F32 ? 4 : 8;
+  const int64_t wa = std::min<int64_t>(params->rank + params->oversample, std::min(m, k));
+  const int64_t wb = std::min<int64_t>(params->rank + params->oversample, std::min(k, n));
+  size_t ws = lramm_ws_bytes(m, k, n, *params, in_dtype);
+  size_t need = (size_t)round_up((m * k + k * n) * es, 256) + round_up((k * wa + n * wb) * 8, 256) +
+                round_up(m * n * ds, 256) + (cmat ? round_up(m * n * cs, 256) : 0) + ws + 8192;
+  LRAMM_TRY(host_reserve(c, need));
+  Arena ar(c.buf, c.cap);
+  char *da = ar.take<char>(m * k * es), *db = ar.take<char>(k * n * es);
+  double *oa = ar.take<double>(k * wa), *ob = ar.take<double>(n * wb);
+  char *dd = ar.take<char>(m * n * ds);
+  char *dc = cmat ? ar.take<char>(m * n * cs) : nullptr;
+  void *w = ar.take<char>((int64_t)ws);
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(da, a, m * k * es, cudaMemcpyHostToDevice, c.st));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(db, b, k * n * es, cudaMemcpyHostToDevice, c.st));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(oa, omega_a, k * wa * 8, cudaMemcpyHostToDevice, c.st));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(ob, omega_b, n * wb * 8, cudaMemcpyHostToDevice, c.st));
+  if (cmat) LRAMM_CUDA_TRY(cudaMemcpyAsync(dc, cmat, m * n * cs, cudaMemcpyHostToDevice, c.st));
+  LRAMM_TRY(lramm_device(da, db, in_dtype, m, k, n, *params, oa, ob, dc, c_dtype, dd, d_dtype, c.status, w, ws,
+                         timings, c.st));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(d, dd, m * n * ds, cudaMemcpyDeviceToHost, c.st));
+  return finish(c);
+}
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+// Shared helpers: status handling, numeric conventions, sm_100a PTX wrappers.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/lramm_cuda.h"
+
+namespace lramm {
+
+// ------------------------------------------------------------------ status
+void set_error(const char *fmt, ...);
+int fail(int code, const char *fmt, ...);
+
+#define LRAMM_CUDA_TRY(expr)                                                              \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return ::lramm::fail(LRAMM_ERR_CUDA, "%s failed: %s (%s:%d)", #expr,                  \
+                           cudaGetErrorString(_e), __FILE__, __LINE__);                     \
+  } while (0)
+
+#define LRAMM_TRY(expr)        \
+  do {                         \
+    int _s = (expr);           \
+    if (_s != LRAMM_OK) return _s; \
+  } while (0)
+
+#define LRAMM_LAUNCH_CHECK() LRAMM_CUDA_TRY(cudaGetLastError())
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+inline int bit_cap(int bits) { return (1 << (bits - 1)) - 1; }  // quant.py:20-22
+
+int num_sms();
+
+// Bump allocator over a caller-provided workspace (256-byte aligned slices).
+struct Arena {
+  char *base = nullptr;
+  size_t cap = 0, off = 0;
+  bool dry = false;  // sizing pass: count bytes only
+  Arena() = default;
+  Arena(void *p, size_t n) : base((char *)p), cap(n), dry(p == nullptr) {}
+  template <class T>
+  T *take(int64_t count) {
+    size_t bytes = round_up((int64_t)(count * sizeof(T)), 256);
+    size_t at = off;
+    off += bytes;
+    if (dry) return nullptr;
+    if (off > cap) return nullptr;
+    return reinterpret_cast<T *>(base + at);
+  }
+  bool ok() const { return dry || off <= cap; }
+};
+
+// ------------------------------------------------------------------ device numerics
+// Bit-exact conventions: every rounding step is an explicit
+// IEEE round-to-nearest intrinsic so nvcc cannot contract it into an FMA.
+__device__ __forceinline__ unsigned long long dbits(double x) { return __double_as_longlong(x); }
+
+// non-negative doubles order like their bit patterns -> atomicMax on u64 is an exact max
+__device__ __forceinline__ void atomic_max_nonneg(double *addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// rint(a*scale) (half-to-even), clamp to +-cap: _core.pyx:63-68
+__device__ __forceinline__ int quant_round(double a, double scale, int cap) {
+  double t = __dmul_rn(a, scale);
+  double r = rint(t);
+  if (r > (double)cap) r = (double)cap;
+  if (r < -(double)cap) r = -(double)cap;
+  return (int)r;
+}
+
+// scale = cap / amax (quant.py:69), all-zero sentinel 1.0 (quant.py:67-68)
+__device__ __forceinline__ double quant_scale(double amax, int cap) {
+  return amax == 0.0 ? 1.0 : __ddiv_rn((double)cap, amax);
+}
+
+template <class T>
+__device__ __forceinline__ double to_f64(T v) { return (double)v; }
+
+}  // namespace lramm

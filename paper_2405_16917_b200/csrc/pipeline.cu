@@ -1,0 +1,461 @@
+// Native orchestration of the hot path: the randomised SVD of each operand
+// (rsvd.py:47-94) and the three-stage recombination (pipeline.py:159-214), as a
+// stream-ordered sequence of sm_100a kernels over caller-provided workspace.
+// No host synchronisation, no allocation: a whole lramm() call can be captured
+// in a CUDA graph.
+//
+// Modes:
+//   parity: sketch / power / projection products in fp64 (the reference),
+//   fast:   those products as int8 tensor-core GEMMs of per-tensor or per-row
+//           quantised operands, dequantised bit-exactly in the epilogue.
+// In both modes the thin QRs (CholeskyQR2), the small SVD (one-sided Jacobi)
+// and the lift are fp64, and the recombination E1 -> E2 -> E3 uses the
+// reference's per-tensor quantiser at (d1, d2, d3) with int8 tcgen05 GEMMs.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace lramm {
+
+int quantize_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits, int gran,
+                    int transpose, void *q, int q_dtype, int64_t ldq, double *scales, int *nonfinite, void *ws,
+                    size_t ws_bytes, cudaStream_t st);
+size_t quantize_ws_bytes(int64_t rows, int64_t cols);
+int igemm_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, const int8_t *b, int64_t ldb,
+                 const lramm_epilogue_t &epi, int split_k, cudaStream_t st);
+int epilogue_device(const int32_t *acc, int64_t M, int64_t N, int64_t lda, const lramm_epilogue_t &epi,
+                    cudaStream_t st);
+int pick_bn(int64_t N);
+int dgemm_device(int trans_a, int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B,
+                 int64_t ldb, double *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st);
+size_t dgemm_ws_bytes(int trans_a, int64_t M, int64_t N, int64_t K);
+int qr_device(const double *y, int64_t m, int64_t w, int64_t ldy, double *q, int64_t ldq, double *r, void *ws,
+              size_t ws_bytes, cudaStream_t st);
+size_t qr_ws_bytes(int64_t m, int64_t w);
+int svd_tall_device(const double *T, int64_t m, int64_t n, int64_t ldt, double *pside, int64_t ldp, double *s,
+                    double *h, int64_t ldh, int *info, int *status, void *ws, size_t ws_bytes, cudaStream_t st);
+size_t svd_tall_ws_bytes(int64_t m, int64_t n);
+
+namespace {
+
+__global__ void f32_to_f64_kernel(const float *__restrict__ x, int64_t n, double *__restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (double)x[i];
+}
+
+// B[i][j] = A[i][j] * s[j]  (u * sigma, pipeline.py:189-190; one IEEE rounding)
+__global__ void scale_cols_kernel(const double *__restrict__ A, int64_t rows, int cols, int64_t lda,
+                                  const double *__restrict__ s, double *__restrict__ B, int64_t ldb) {
+  int64_t n = rows * cols;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / cols;
+    int c = (int)(i - r * cols);
+    B[r * ldb + c] = __dmul_rn(A[r * lda + c], s[c]);
+  }
+}
+
+// status summary: jacobi info (<0 = no convergence), non-finite flag, completion status
+__global__ void summarize_status_kernel(const int *jac_info, int njac, const int *nonfinite, const int *compl_st,
+                                        int *status) {
+  if (threadIdx.x != 0) return;
+  int s = 0;
+  for (int i = 0; i < njac && !s; ++i)
+    if (jac_info[i] < 0) s = LRAMM_ERR_NONCONVERGENCE;
+  if (!s && compl_st && *compl_st) s = *compl_st;
+  if (nonfinite && *nonfinite) s = LRAMM_ERR_NONFINITE;
+  *status = s;
+}
+
+inline int elem_grid(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 8LL * num_sms())); }
+
+struct QOp {  // a quantised K-major operand
+  int8_t *q = nullptr;
+  int64_t ld = 0;
+  double *scale = nullptr;
+  int64_t inc = 0;
+};
+
+struct RsvdBufs {
+  int64_t rows = 0, cols = 0, w = 0, r = 0;
+  bool fast = false;
+  int gran = LRAMM_GRAN_TENSOR;
+  // fast-mode operands
+  QOp xr_s, xr_p, xc_p, xc_j, om, qq, qzq;
+  // parity mode fp64 copy of x (when x is fp32)
+  double *x64 = nullptr;
+  double *Y = nullptr, *Q = nullptr, *Z = nullptr, *Qz = nullptr, *BsT = nullptr, *Pside = nullptr, *H = nullptr,
+         *s = nullptr;
+  int32_t *acc = nullptr;
+  int *info = nullptr, *compl_st = nullptr, *nonfinite = nullptr;
+  void *qr_ws = nullptr, *svd_ws = nullptr, *gemm_ws = nullptr, *qz_ws = nullptr;
+  size_t qr_bytes = 0, svd_bytes = 0, gemm_bytes = 0, qz_bytes = 0;
+};
+
+QOp take_qop(Arena &ar, int64_t rows, int64_t kdim, int64_t nscale) {
+  QOp o;
+  o.ld = round_up(kdim, 16);
+  o.q = ar.take<int8_t>(rows * o.ld);
+  o.scale = ar.take<double>(nscale);
+  o.inc = nscale > 1 ? 1 : 0;
+  return o;
+}
+
+RsvdBufs carve_rsvd(Arena &ar, int64_t rows, int64_t cols, int x_dtype, const lramm_params_t &P) {
+  RsvdBufs b;
+  b.rows = rows;
+  b.cols = cols;
+  b.r = P.rank;
+  b.w = std::min<int64_t>(P.rank + P.oversample, std::min(rows, cols));
+  b.fast = P.mode == LRAMM_MODE_FAST;
+  b.gran = P.granularity == LRAMM_GRAN_ROW ? LRAMM_GRAN_ROW : LRAMM_GRAN_TENSOR;
+  const bool row = b.gran == LRAMM_GRAN_ROW;
+  const int64_t w = b.w;
+  if (b.fast) {
+    b.xr_s = take_qop(ar, rows, cols, row ? rows : 1);
+    if (P.power_iters > 0) b.xr_p = P.power_bits == P.sketch_bits ? b.xr_s : take_qop(ar, rows, cols, row ? rows : 1);
+    b.xc_j = take_qop(ar, cols, rows, row ? cols : 1);
+    if (P.power_iters > 0) b.xc_p = P.power_bits == P.proj_bits ? b.xc_j : take_qop(ar, cols, rows, row ? cols : 1);
+    b.om = take_qop(ar, w, cols, row ? w : 1);
+    b.qq = take_qop(ar, w, rows, row ? w : 1);
+    b.qzq = take_qop(ar, w, cols, row ? w : 1);
+    b.qz_bytes = quantize_ws_bytes(std::max(rows, cols), std::max(rows, cols));
+    b.qz_ws = ar.take<char>((int64_t)b.qz_bytes);
+    int64_t mx = std::max(rows, cols);
+    b.acc = ar.take<int32_t>(mx * w);
+  } else if (x_dtype == LRAMM_F32) {
+    b.x64 = ar.take<double>(rows * cols);
+  }
+  b.Y = ar.take<double>(rows * w);
+  b.Q = ar.take<double>(rows * w);
+  b.Z = ar.take<double>(cols * w);
+  b.Qz = ar.take<double>(cols * w);
+  b.BsT = ar.take<double>(cols * w);
+  b.Pside = ar.take<double>(cols * w);
+  b.H = ar.take<double>(w * w);
+  b.s = ar.take<double>(w);
+  b.info = ar.take<int>(4);
+  b.compl_st = ar.take<int>(4);
+  b.nonfinite = ar.take<int>(4);
+  int64_t mx = std::max(rows, cols);
+  b.qr_bytes = qr_ws_bytes(mx, w);
+  b.qr_ws = ar.take<char>((int64_t)b.qr_bytes);
+  b.svd_bytes = svd_tall_ws_bytes(cols, w);
+  b.svd_ws = ar.take<char>((int64_t)b.svd_bytes);
+  b.gemm_bytes = std::max(dgemm_ws_bytes(1, cols, w, rows), dgemm_ws_bytes(0, rows, w, cols));
+  b.gemm_bytes = std::max(b.gemm_bytes, dgemm_ws_bytes(0, rows, P.rank, w));
+  b.gemm_ws = ar.take<char>((int64_t)b.gemm_bytes);
+  return b;
+}
+
+// C (M x N fp64) = dequant(A . B^T): row scales of A, column scales of B
+int qprod(const QOp &A, const QOp &B, int64_t M, int64_t N, int64_t K, double *C, int64_t ldc, int transpose_out,
+          int32_t *acc, cudaStream_t st) {
+  lramm_epilogue_t e = {};
+  e.out_dtype = LRAMM_F64;
+  e.transpose_out = transpose_out;
+  e.out = C;
+  e.ldo = ldc;
+  e.row_scale = A.scale;
+  e.row_scale_inc = A.inc;
+  e.col_scale = B.scale;
+  e.col_scale_inc = B.inc;
+  e.alpha = 1.0;
+  e.beta = 0.0;
+  const int64_t tiles = ceil_div(M, 128) * ceil_div(N, pick_bn(N));
+  const int64_t kb = ceil_div(K, 128);
+  int split = 1;
+  if (acc && tiles * 2 < num_sms() && kb >= 8) split = (int)std::min<int64_t>(kb / 4, ceil_div(num_sms(), tiles));
+  if (split <= 1) return igemm_device(M, N, K, A.q, A.ld, B.q, B.ld, e, 1, st);
+  LRAMM_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)M * N * sizeof(int32_t), st));
+  lramm_epilogue_t ea = {};
+  ea.out_dtype = LRAMM_I32;
+  ea.accumulate = 1;
+  ea.out = acc;
+  ea.ldo = N;
+  LRAMM_TRY(igemm_device(M, N, K, A.q, A.ld, B.q, B.ld, ea, split, st));
+  return epilogue_device(acc, M, N, N, e, st);
+}
+
+int quant(const void *x, int dtype, int64_t rows, int64_t cols, int64_t ldx, int bits, int gran, int transpose,
+          QOp &o, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st) {
+  return quantize_device(x, dtype, rows, cols, ldx, bits, gran, transpose, o.q, LRAMM_I8, o.ld, o.scale, nonfinite,
+                         ws, ws_bytes, st);
+}
+
+int check_bits_dev(int bits, const char *what) {
+  if (bits < 2 || bits > 24) return fail(LRAMM_ERR_PARAM, "%s must be an integer in [2, 24], got %d", what, bits);
+  if (bits > 8)
+    return fail(LRAMM_ERR_UNSUPPORTED, "%s = %d: the int8 tensor-core path supports bit budgets <= 8", what, bits);
+  return LRAMM_OK;
+}
+
+// int32 accumulation guard: K * cap_a * cap_b < 2^31 (the reference's int64 guard is quant.py:87-93)
+int check_acc(int64_t K, int bits_a, int bits_b) {
+  if ((double)K * bit_cap(bits_a) * bit_cap(bits_b) >= 2147483648.0)
+    return fail(LRAMM_ERR_OVERFLOW, "k=%lld with bit budgets (%d, %d) risks int32 accumulator overflow",
+                (long long)K, bits_a, bits_b);
+  return LRAMM_OK;
+}
+
+int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, const double *omega, double *U,
+             int64_t ldu, double *S, double *V, int64_t ldv, cudaStream_t st) {
+  const int64_t rows = b.rows, cols = b.cols, w = b.w, r = b.r;
+  LRAMM_CUDA_TRY(cudaMemsetAsync(b.info, 0, 4 * sizeof(int), st));
+  LRAMM_CUDA_TRY(cudaMemsetAsync(b.compl_st, 0, 4 * sizeof(int), st));
+  LRAMM_CUDA_TRY(cudaMemsetAsync(b.nonfinite, 0, 4 * sizeof(int), st));
+  const int gran_l = b.gran == LRAMM_GRAN_ROW ? LRAMM_GRAN_ROW : LRAMM_GRAN_TENSOR;  // left operand rows
+  const int gran_r = b.gran == LRAMM_GRAN_ROW ? LRAMM_GRAN_COL : LRAMM_GRAN_TENSOR;  // right operand columns
+  const double *x64 = (const double *)x;
+  if (b.fast) {
+    // Y = X . Omega at sketch_bits
+    LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.sketch_bits, gran_l, 0, b.xr_s, b.nonfinite, b.qz_ws, b.qz_bytes, st));
+    LRAMM_TRY(quant(omega, LRAMM_F64, cols, w, w, P.sketch_bits, gran_r, 1, b.om, nullptr, b.qz_ws, b.qz_bytes, st));
+    LRAMM_TRY(qprod(b.xr_s, b.om, rows, w, cols, b.Y, w, 0, b.acc, st));
+  } else {
+    if (x_dtype == LRAMM_F32) {
+      f32_to_f64_kernel<<<elem_grid(rows * cols), 256, 0, st>>>((const float *)x, rows * cols, b.x64);
+      LRAMM_LAUNCH_CHECK();
+      x64 = b.x64;
+    }
+    LRAMM_TRY(dgemm_device(0, rows, w, cols, x64, cols, omega, w, b.Y, w, b.gemm_ws, b.gemm_bytes, st));
+  }
+  LRAMM_TRY(qr_device(b.Y, rows, w, w, b.Q, w, nullptr, b.qr_ws, b.qr_bytes, st));
+  if (b.fast && P.power_iters > 0) {
+    if (b.xr_p.q != b.xr_s.q)
+      LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.power_bits, gran_l, 0, b.xr_p, b.nonfinite, b.qz_ws, b.qz_bytes, st));
+    LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.power_bits, gran_r == LRAMM_GRAN_COL ? LRAMM_GRAN_COL : LRAMM_GRAN_TENSOR,
+                    1, b.xc_p, b.nonfinite, b.qz_ws, b.qz_bytes, st));
+  }
+  for (int it = 0; it < P.power_iters; ++it) {
+    // Z = X^T Q ; Qz = qr(Z) ; Y = X Qz ; Q = qr(Y)   (rsvd.py:60-64)
+    if (b.fast) {
+      LRAMM_TRY(quant(b.Q, LRAMM_F64, rows, w, w, P.power_bits, gran_r, 1, b.qq, nullptr, b.qz_ws, b.qz_bytes, st));
+      LRAMM_TRY(qprod(b.xc_p, b.qq, cols, w, rows, b.Z, w, 0, b.acc, st));
+    } else {
+      LRAMM_TRY(dgemm_device(1, cols, w, rows, x64, cols, b.Q, w, b.Z, w, b.gemm_ws, b.gemm_bytes, st));
+    }
+    LRAMM_TRY(qr_device(b.Z, cols, w, w, b.Qz, w, nullptr, b.qr_ws, b.qr_bytes, st));
+    if (b.fast) {
+      LRAMM_TRY(quant(b.Qz, LRAMM_F64, cols, w, w, P.power_bits, gran_r, 1, b.qzq, nullptr, b.qz_ws, b.qz_bytes, st));
+      LRAMM_TRY(qprod(b.xr_p, b.qzq, rows, w, cols, b.Y, w, 0, b.acc, st));
+    } else {
+      LRAMM_TRY(dgemm_device(0, rows, w, cols, x64, cols, b.Qz, w, b.Y, w, b.gemm_ws, b.gemm_bytes, st));
+    }
+    LRAMM_TRY(qr_device(b.Y, rows, w, w, b.Q, w, nullptr, b.qr_ws, b.qr_bytes, st));
+  }
+  // Bs^T = X^T Q   (rsvd.py:77, evaluated transposed)
+  if (b.fast) {
+    if (b.xc_j.q != b.xc_p.q || P.power_iters == 0)
+      LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.proj_bits, gran_r == LRAMM_GRAN_COL ? LRAMM_GRAN_COL : LRAMM_GRAN_TENSOR,
+                      1, b.xc_j, b.nonfinite, b.qz_ws, b.qz_bytes, st));
+    LRAMM_TRY(quant(b.Q, LRAMM_F64, rows, w, w, P.proj_bits, gran_r, 1, b.qq, nullptr, b.qz_ws, b.qz_bytes, st));
+    LRAMM_TRY(qprod(b.xc_j, b.qq, cols, w, rows, b.BsT, w, 0, b.acc, st));
+  } else {
+    LRAMM_TRY(dgemm_device(1, cols, w, rows, x64, cols, b.Q, w, b.BsT, w, b.gemm_ws, b.gemm_bytes, st));
+  }
+  // SVD(Bs): u = H, v = Bs^T H diag(s)^-1   (rsvd.py:78, _jacobi.py)
+  LRAMM_TRY(svd_tall_device(b.BsT, cols, w, w, b.Pside, w, b.s, b.H, w, b.info, b.compl_st, b.svd_ws, b.svd_bytes, st));
+  // lift U = Q u (rsvd.py:79) and truncate (rsvd.py:84-94)
+  LRAMM_TRY(dgemm_device(0, rows, r, w, b.Q, w, b.H, w, U, ldu, b.gemm_ws, b.gemm_bytes, st));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(S, b.s, r * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  LRAMM_CUDA_TRY(cudaMemcpy2DAsync(V, ldv * sizeof(double), b.Pside, w * sizeof(double), r * sizeof(double), cols,
+                                   cudaMemcpyDeviceToDevice, st));
+  return LRAMM_OK;
+}
+
+int validate_params(const lramm_params_t &P, bool need_bits) {
+  if (P.rank < 1) return fail(LRAMM_ERR_PARAM, "rank must be >= 1, got %d", P.rank);
+  if (P.power_iters < 0 || P.oversample < 0) return fail(LRAMM_ERR_PARAM, "power_iters and oversample must be >= 0");
+  if (P.mode != LRAMM_MODE_PARITY && P.mode != LRAMM_MODE_FAST) return fail(LRAMM_ERR_PARAM, "bad mode %d", P.mode);
+  if (P.mode == LRAMM_MODE_FAST) {
+    LRAMM_TRY(check_bits_dev(P.sketch_bits, "sketch_bits"));
+    LRAMM_TRY(check_bits_dev(P.proj_bits, "proj_bits"));
+    if (P.power_iters > 0) LRAMM_TRY(check_bits_dev(P.power_bits, "power_bits"));
+  }
+  if (need_bits)
+    for (int i = 0; i < 3; ++i) LRAMM_TRY(check_bits_dev(P.bits[i], "bits"));
+  return LRAMM_OK;
+}
+
+struct LrammBufs {
+  RsvdBufs ra, rb;
+  double *UA, *SA, *VA, *UB, *SB, *VB, *E1, *Zsc, *E2T, *Usc;
+  QOp vt, wq, e1q, zq, e2q, uq;
+  int32_t *e1acc;
+  int *nonfinite, *jinfo;
+  void *qws;
+  size_t qbytes;
+};
+
+LrammBufs carve_lramm(Arena &ar, int64_t m, int64_t k, int64_t n, int in_dtype, const lramm_params_t &P) {
+  LrammBufs L;
+  const int64_t r = P.rank;
+  L.ra = carve_rsvd(ar, m, k, in_dtype, P);
+  L.rb = carve_rsvd(ar, k, n, in_dtype, P);
+  L.UA = ar.take<double>(m * r);
+  L.SA = ar.take<double>(r);
+  L.VA = ar.take<double>(k * r);
+  L.UB = ar.take<double>(k * r);
+  L.SB = ar.take<double>(r);
+  L.VB = ar.take<double>(n * r);
+  L.E1 = ar.take<double>(r * r);
+  L.Zsc = ar.take<double>(n * r);
+  L.E2T = ar.take<double>(n * r);
+  L.Usc = ar.take<double>(m * r);
+  L.vt = take_qop(ar, r, k, 1);
+  L.wq = take_qop(ar, r, k, 1);
+  L.e1q = take_qop(ar, r, r, 1);
+  L.zq = take_qop(ar, n, r, 1);
+  L.e2q = take_qop(ar, n, r, 1);
+  L.uq = take_qop(ar, m, r, 1);
+  L.e1acc = ar.take<int32_t>(r * r);
+  L.nonfinite = ar.take<int>(4);
+  L.jinfo = ar.take<int>(4);
+  int64_t mx = std::max(std::max(m, n), k);
+  L.qbytes = quantize_ws_bytes(mx, mx);
+  L.qws = ar.take<char>((int64_t)L.qbytes);
+  return L;
+}
+
+__global__ void gather_info_kernel(const int *a, const int *b, const int *ca, const int *cb, const int *nfa,
+                                   const int *nfb, int *jinfo, int *nonfinite) {
+  if (threadIdx.x) return;
+  jinfo[0] = a[0];
+  jinfo[1] = b[0];
+  jinfo[2] = ca[0] ? -1 : 0;
+  jinfo[3] = cb[0] ? -1 : 0;
+  if (nfa[0] || nfb[0]) nonfinite[0] = 1;
+}
+
+}  // namespace
+
+size_t rsvd_ws_bytes(int64_t rows, int64_t cols, const lramm_params_t &P, int x_dtype) {
+  Arena ar;
+  ar.dry = true;
+  carve_rsvd(ar, rows, cols, x_dtype, P);
+  return ar.off + 1024;
+}
+
+int rsvd_device(const void *x, int x_dtype, int64_t rows, int64_t cols, const lramm_params_t &P, const double *omega,
+                double *U, double *S, double *V, int *status, void *ws, size_t ws_bytes, cudaStream_t st) {
+  LRAMM_TRY(validate_params(P, false));
+  if (x_dtype != LRAMM_F32 && x_dtype != LRAMM_F64) return fail(LRAMM_ERR_PARAM, "rsvd: x must be F32 or F64");
+  if (rows < 1 || cols < 1) return fail(LRAMM_ERR_SHAPE, "rsvd: empty matrix");
+  if (P.rank > std::min(rows, cols))
+    return fail(LRAMM_ERR_PARAM, "rank %d exceeds min dim %lld", P.rank, (long long)std::min(rows, cols));
+  Arena ar(ws, ws_bytes);
+  RsvdBufs b = carve_rsvd(ar, rows, cols, x_dtype, P);
+  if (!ar.ok()) return fail(LRAMM_ERR_WORKSPACE, "rsvd: workspace too small (%zu needed)", ar.off);
+  if (b.fast) {
+    LRAMM_TRY(check_acc(cols, P.sketch_bits, P.sketch_bits));
+    LRAMM_TRY(check_acc(rows, P.proj_bits, P.proj_bits));
+    if (P.power_iters > 0) LRAMM_TRY(check_acc(std::max(rows, cols), P.power_bits, P.power_bits));
+  }
+  LRAMM_TRY(run_rsvd(x, x_dtype, b, P, omega, U, P.rank, S, V, P.rank, st));
+  summarize_status_kernel<<<1, 32, 0, st>>>(b.info, 1, b.nonfinite, b.compl_st, status);
+  LRAMM_LAUNCH_CHECK();
+  return LRAMM_OK;
+}
+
+size_t lramm_ws_bytes(int64_t m, int64_t k, int64_t n, const lramm_params_t &P, int in_dtype) {
+  Arena ar;
+  ar.dry = true;
+  carve_lramm(ar, m, k, n, in_dtype, P);
+  return ar.off + 1024;
+}
+
+int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t k, int64_t n, const lramm_params_t &P,
+                 const double *omega_a, const double *omega_b, const void *c, int c_dtype, void *d, int d_dtype,
+                 int *status, void *ws, size_t ws_bytes, lramm_timings_t *timings, cudaStream_t st) {
+  LRAMM_TRY(validate_params(P, true));
+  if (P.rank < 2) return fail(LRAMM_ERR_PARAM, "rank must be >= 2, got %d", P.rank);
+  if (in_dtype != LRAMM_F32 && in_dtype != LRAMM_F64) return fail(LRAMM_ERR_PARAM, "inputs must be F32 or F64");
+  if (d_dtype != LRAMM_F32 && d_dtype != LRAMM_F64) return fail(LRAMM_ERR_PARAM, "output must be F32 or F64");
+  if (m < 1 || k < 1 || n < 1) return fail(LRAMM_ERR_SHAPE, "empty operand");
+  if (P.rank > std::min(m, k) || P.rank > std::min(k, n))
+    return fail(LRAMM_ERR_PARAM, "rank %d exceeds operand min dims %lld, %lld", P.rank, (long long)std::min(m, k),
+                (long long)std::min(k, n));
+  const int64_t r = P.rank;
+  const int d1 = P.bits[0], d2 = P.bits[1], d3 = P.bits[2];
+  LRAMM_TRY(check_acc(k, d1, d1));
+  LRAMM_TRY(check_acc(r, d2, d2));
+  LRAMM_TRY(check_acc(r, d3, d3));
+  if (P.mode == LRAMM_MODE_FAST) {
+    int64_t mx = std::max(std::max(m, n), k);
+    LRAMM_TRY(check_acc(mx, P.sketch_bits, P.sketch_bits));
+    LRAMM_TRY(check_acc(mx, P.proj_bits, P.proj_bits));
+    if (P.power_iters > 0) LRAMM_TRY(check_acc(mx, P.power_bits, P.power_bits));
+  }
+  Arena ar(ws, ws_bytes);
+  LrammBufs L = carve_lramm(ar, m, k, n, in_dtype, P);
+  if (!ar.ok()) return fail(LRAMM_ERR_WORKSPACE, "lramm: workspace too small (%zu needed)", ar.off);
+
+  cudaEvent_t ev[6] = {};
+  if (timings)
+    for (int i = 0; i < 6; ++i) LRAMM_CUDA_TRY(cudaEventCreate(&ev[i]));
+  auto mark = [&](int i) -> int {
+    if (timings) LRAMM_CUDA_TRY(cudaEventRecord(ev[i], st));
+    return LRAMM_OK;
+  };
+  LRAMM_TRY(mark(0));
+  // ---- rsvd of both operands (pipeline.py:183-186)
+  LRAMM_TRY(run_rsvd(a, in_dtype, L.ra, P, omega_a, L.UA, r, L.SA, L.VA, r, st));
+  LRAMM_TRY(run_rsvd(b, in_dtype, L.rb, P, omega_b, L.UB, r, L.SB, L.VB, r, st));
+  LRAMM_TRY(mark(1));
+  // ---- scaling (pipeline.py:188-193): Usc = U_A sigma_A, Zsc^T = V_B sigma_B
+  scale_cols_kernel<<<elem_grid(m * r), 256, 0, st>>>(L.UA, m, (int)r, r, L.SA, L.Usc, r);
+  LRAMM_LAUNCH_CHECK();
+  scale_cols_kernel<<<elem_grid(n * r), 256, 0, st>>>(L.VB, n, (int)r, r, L.SB, L.Zsc, r);
+  LRAMM_LAUNCH_CHECK();
+  LRAMM_TRY(mark(2));
+  LRAMM_CUDA_TRY(cudaMemsetAsync(L.nonfinite, 0, 4 * sizeof(int), st));
+  // ---- E1 = QM(V_A^T U_B, d1)   (r x r, K = k)
+  LRAMM_TRY(quant(L.VA, LRAMM_F64, k, r, r, d1, LRAMM_GRAN_TENSOR, 1, L.vt, L.nonfinite, L.qws, L.qbytes, st));
+  LRAMM_TRY(quant(L.UB, LRAMM_F64, k, r, r, d1, LRAMM_GRAN_TENSOR, 1, L.wq, L.nonfinite, L.qws, L.qbytes, st));
+  LRAMM_TRY(qprod(L.vt, L.wq, r, r, k, L.E1, r, 0, L.e1acc, st));
+  LRAMM_TRY(mark(3));
+  // ---- E2 = QM(E1 Zsc, d2)   (r x n, K = r) stored transposed for E3
+  LRAMM_TRY(quant(L.E1, LRAMM_F64, r, r, r, d2, LRAMM_GRAN_TENSOR, 0, L.e1q, L.nonfinite, L.qws, L.qbytes, st));
+  LRAMM_TRY(quant(L.Zsc, LRAMM_F64, n, r, r, d2, LRAMM_GRAN_TENSOR, 0, L.zq, L.nonfinite, L.qws, L.qbytes, st));
+  LRAMM_TRY(qprod(L.e1q, L.zq, r, n, r, L.E2T, r, 1, nullptr, st));
+  LRAMM_TRY(mark(4));
+  // ---- E3 = QM(Usc E2, d3) ; D = alpha E3 + beta C   (m x n, K = r)
+  LRAMM_TRY(quant(L.Usc, LRAMM_F64, m, r, r, d3, LRAMM_GRAN_TENSOR, 0, L.uq, L.nonfinite, L.qws, L.qbytes, st));
+  LRAMM_TRY(quant(L.E2T, LRAMM_F64, n, r, r, d3, LRAMM_GRAN_TENSOR, 0, L.e2q, L.nonfinite, L.qws, L.qbytes, st));
+  {
+    lramm_epilogue_t e = {};
+    e.out_dtype = d_dtype;
+    e.out = d;
+    e.ldo = n;
+    e.row_scale = L.uq.scale;
+    e.row_scale_inc = 0;
+    e.col_scale = L.e2q.scale;
+    e.col_scale_inc = 0;
+    e.alpha = P.alpha;
+    e.beta = c ? P.beta : 0.0;
+    e.c = c;
+    e.c_dtype = c_dtype;
+    e.ldc = n;
+    LRAMM_TRY(igemm_device(m, n, r, L.uq.q, L.uq.ld, L.e2q.q, L.e2q.ld, e, 1, st));
+  }
+  LRAMM_TRY(mark(5));
+  gather_info_kernel<<<1, 32, 0, st>>>(L.ra.info, L.rb.info, L.ra.compl_st, L.rb.compl_st, L.ra.nonfinite,
+                                       L.rb.nonfinite, L.jinfo, L.nonfinite);
+  LRAMM_LAUNCH_CHECK();
+  summarize_status_kernel<<<1, 32, 0, st>>>(L.jinfo, 4, L.nonfinite, nullptr, status);
+  LRAMM_LAUNCH_CHECK();
+  if (timings) {
+    LRAMM_CUDA_TRY(cudaEventSynchronize(ev[5]));
+    float t[5];
+    for (int i = 0; i < 5; ++i) LRAMM_CUDA_TRY(cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]));
+    timings->rsvd_ms = t[0];
+    timings->scaling_ms = t[1];
+    timings->gemm1_ms = t[2];
+    timings->gemm2_ms = t[3];
+    timings->gemm3_ms = t[4];
+    for (int i = 0; i < 6; ++i) cudaEventDestroy(ev[i]);
+  }
+  return LRAMM_OK;
+}
+
+}  // namespace lramm

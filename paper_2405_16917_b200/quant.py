@@ -1,0 +1,202 @@
+"""Symmetric linear quantiser and integer quantised GEMM on sm_100a.
+
+Same public surface and semantics as the reference's `quant.py`
+(`quantize` :55-71, `dequantize` :74-76, `integer_matmul` :79-84, `qgemm` :96-121):
+scale = (2^(bits-1)-1) / max|a| in fp64, rint half-to-even, clamp, sentinel
+scale 1.0 for all-zero input, dequantisation acc / (sa*sb).  Integer data and
+scales are bit-identical to the reference's; products run as int8 tcgen05 GEMMs
+(bit budgets <= 8) with int32 accumulation.
+
+Inputs may be NumPy arrays (results come back as NumPy, the reference's types)
+or CUDA tensors (results stay on the device).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._device import WORKSPACE, dtype_code, ptr, require_device, stream_handle, to_device_matrix
+from .errors import OverflowRiskError, ParameterError, ShapeError, UnsupportedError
+
+BITS_MIN = 2
+BITS_MAX = 24
+MMA_BITS_MAX = 8  # int8 tensor-core operands
+
+
+def bit_cap(bits):
+    """Largest representable magnitude for a bit budget: 2^(bits-1) - 1 (quant.py:20-22)."""
+    return (1 << (bits - 1)) - 1
+
+
+def _check_bits(bits, name="bits"):
+    if not isinstance(bits, (int, np.integer)) or not BITS_MIN <= int(bits) <= BITS_MAX:
+        raise ParameterError(f"{name} must be an integer in [{BITS_MIN}, {BITS_MAX}], got {bits}")
+    return int(bits)
+
+
+@dataclass(frozen=True)
+class QuantizedMatrix:
+    """Integer matrix plus its quantizer scale and bit budget (quant.py:31-52)."""
+
+    data: object  # int32 (rows, cols): NumPy array or CUDA tensor
+    bits: int
+    scale: float
+
+    def __post_init__(self):
+        if self.data.ndim != 2 or self.data.dtype not in (np.int32, torch.int32):
+            raise ShapeError("quantized payload must be a 2-D int32 array")
+        _check_bits(self.bits)
+        if not self.scale > 0:
+            raise ParameterError(f"scale must be positive, got {self.scale}")
+
+    @property
+    def rows(self):
+        return self.data.shape[0]
+
+    @property
+    def cols(self):
+        return self.data.shape[1]
+
+
+def _is_cuda(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def _as_2d(a, name):
+    shape = tuple(a.shape) if hasattr(a, "shape") else np.asarray(a).shape
+    if len(shape) != 2:
+        raise ShapeError(f"{name} must be 2-D, got ndim={len(shape)}")
+    if shape[0] < 1 or shape[1] < 1:
+        raise ShapeError(f"{name} must have positive dimensions, got {shape}")
+    return shape
+
+
+def quantize_device(x: torch.Tensor, bits: int, granularity: int = N.GRAN_TENSOR, transpose: bool = False,
+                    out_dtype: int = N.I8, ld: int | None = None):
+    """Device quantiser -> (q tensor, scales fp64 tensor, nonfinite flag tensor)."""
+    dev = x.device
+    rows, cols = x.shape
+    out_rows, out_cols = (cols, rows) if transpose else (rows, cols)
+    if ld is None:
+        ld = ((out_cols + 15) // 16) * 16 if out_dtype == N.I8 else out_cols
+    tdt = {N.I8: torch.int8, N.I32: torch.int32}[out_dtype]
+    q = torch.empty((out_rows, ld), dtype=tdt, device=dev)
+    nscale = 1 if granularity == N.GRAN_TENSOR else (rows if granularity == N.GRAN_ROW else cols)
+    scales = torch.empty(nscale, dtype=torch.float64, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    wsz = N.LIB.lramm_quantize_ws(rows, cols)
+    ws = WORKSPACE.get(wsz, dev)
+    N.check(N.LIB.lramm_quantize(ptr(x), dtype_code(x), rows, cols, x.stride(0), int(bits), granularity,
+                                 int(transpose), ptr(q), out_dtype, ld, ptr(scales), ptr(flag), ptr(ws), wsz,
+                                 stream_handle(dev)))
+    return q, scales, flag
+
+
+def quantize(a, bits):
+    """Quantize to `bits`-wide signed integers with a per-matrix scale (quant.py:55-71)."""
+    _as_2d(a, "matrix")
+    bits = _check_bits(bits)
+    on_dev = _is_cuda(a)
+    dev = require_device(a.device if on_dev else None)
+    x = to_device_matrix(a, dev)
+    q, scales, flag = quantize_device(x, bits, N.GRAN_TENSOR, False, N.I32)
+    if int(flag.item()):
+        raise ParameterError("cannot quantize non-finite entries")
+    scale = float(scales.item())
+    data = q if on_dev else q.cpu().numpy()
+    return QuantizedMatrix(data, bits, scale)
+
+
+def dequantize(q):
+    """Map integers back to float64: entries / scale (quant.py:74-76)."""
+    if _is_cuda(q.data):
+        return q.data.to(torch.float64) / q.scale
+    dev = require_device()
+    return (torch.from_numpy(np.ascontiguousarray(q.data)).to(dev).to(torch.float64) / q.scale).cpu().numpy()
+
+
+def _check_overflow(k, bits_a, bits_b):
+    # quant.py:87-93: worst-case |sum| = k * cap_a * cap_b must stay below 2^63
+    if k * bit_cap(bits_a) * bit_cap(bits_b) >= 1 << 63:
+        raise OverflowRiskError(f"k={k} with bit budgets ({bits_a}, {bits_b}) risks int64 overflow")
+    # the tensor-core path accumulates in int32
+    if k * bit_cap(min(bits_a, MMA_BITS_MAX)) * bit_cap(min(bits_b, MMA_BITS_MAX)) >= 1 << 31:
+        raise OverflowRiskError(f"k={k} with bit budgets ({bits_a}, {bits_b}) risks int32 accumulator overflow")
+
+
+def _require_mma_bits(*bits):
+    for b in bits:
+        if b > MMA_BITS_MAX:
+            raise UnsupportedError(f"bit budget {b}: the int8 tensor-core path supports bit budgets <= {MMA_BITS_MAX}")
+
+
+def integer_matmul(qa, qb):
+    """Exact integer product of two quantized matrices, int64 entries (quant.py:79-84)."""
+    if qa.cols != qb.rows:
+        raise ShapeError(f"inner dimensions differ: {tuple(qa.data.shape)} @ {tuple(qb.data.shape)}")
+    _check_overflow(qa.cols, qa.bits, qb.bits)
+    _require_mma_bits(qa.bits, qb.bits)
+    from . import kernels
+
+    a = qa.data.cpu().numpy() if _is_cuda(qa.data) else qa.data
+    b = qb.data.cpu().numpy() if _is_cuda(qb.data) else qb.data
+    out = kernels.imatmul(np.ascontiguousarray(a, dtype=np.int32), np.ascontiguousarray(b, dtype=np.int32))
+    return torch.from_numpy(out).to(qa.data.device) if _is_cuda(qa.data) else out
+
+
+def qgemm_device(a: torch.Tensor, b: torch.Tensor, bits_a: int, bits_b: int, alpha=1.0, beta=0.0, c=None,
+                 out_dtype=torch.float64) -> torch.Tensor:
+    """alpha * dequant(int(A) @ int(B)) + beta * C on device; A: m x k, B: k x n."""
+    dev = a.device
+    m, k = a.shape
+    n = b.shape[1]
+    qa, sa, fa = quantize_device(a, bits_a, N.GRAN_TENSOR, False, N.I8)
+    qb, sb, fb = quantize_device(b, bits_b, N.GRAN_TENSOR, True, N.I8)  # B^T: n x k, K-major
+    out = torch.empty((m, n), dtype=out_dtype, device=dev)
+    e = N.Epilogue()
+    e.out_dtype = N.F64 if out_dtype == torch.float64 else N.F32
+    e.out = out.data_ptr()
+    e.ldo = n
+    e.row_scale = sa.data_ptr()
+    e.row_scale_inc = 0
+    e.col_scale = sb.data_ptr()
+    e.col_scale_inc = 0
+    e.alpha = float(alpha)
+    e.beta = float(beta) if c is not None else 0.0
+    if c is not None:
+        e.c = c.data_ptr()
+        e.c_dtype = dtype_code(c)
+        e.ldc = c.stride(0)
+    N.check(N.LIB.lramm_igemm(m, n, k, ptr(qa), qa.stride(0), ptr(qb), qb.stride(0), ctypes.byref(e), 1,
+                              stream_handle(dev)))
+    if int(fa.item()) or int(fb.item()):
+        raise ParameterError("cannot quantize non-finite entries")
+    return out
+
+
+def qgemm(a, b, bits_a, bits_b, alpha=1.0, beta=0.0, c=None):
+    """Quantized GEMM: alpha * dequant(int(A) @ int(B)) + beta * C (quant.py:96-121)."""
+    sa_shape = _as_2d(a, "a")
+    sb_shape = _as_2d(b, "b")
+    if sa_shape[1] != sb_shape[0]:
+        raise ShapeError(f"inner dimensions differ: {sa_shape} @ {sb_shape}")
+    if c is not None:
+        sc = _as_2d(c, "c")
+        if sc != (sa_shape[0], sb_shape[1]):
+            raise ShapeError(f"c has shape {sc}, expected {(sa_shape[0], sb_shape[1])}")
+    bits_a = _check_bits(bits_a, "bits_a")
+    bits_b = _check_bits(bits_b, "bits_b")
+    _check_overflow(sa_shape[1], bits_a, bits_b)
+    _require_mma_bits(bits_a, bits_b)
+    on_dev = _is_cuda(a)
+    dev = require_device(a.device if on_dev else None)
+    ta = to_device_matrix(a, dev)
+    tb = to_device_matrix(b, dev)
+    tc = to_device_matrix(c, dev) if (c is not None and beta != 0.0) else None
+    out = qgemm_device(ta, tb, bits_a, bits_b, alpha, beta, tc)
+    return out if on_dev else out.cpu().numpy()

@@ -1,0 +1,287 @@
+"""Kernel-level parity on the B200 against the CPU oracle (bit-exact for integer work).
+
+Mirrors the reference's kernel tests (pkg/tests/test_backends.py, test_quant.py):
+quantiser KATs and bit-identity, exact integer products, qgemm dequantisation,
+fp64 GEMM, thin QR and the Jacobi SVD contracts.
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import lramm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def L():
+    import paper_2405_16917_b200 as lib
+
+    return lib
+
+
+@pytest.fixture(scope="module")
+def N():
+    from paper_2405_16917_b200 import _native
+
+    return _native
+
+
+def dev():
+    return torch.device("cuda", 0)
+
+
+# ------------------------------------------------------------------ quantiser
+
+
+def test_quantize_kats(L):
+    q = L.quantize(np.array([[1.0, -1.0]]), 8)  # test_quant.py:32-35
+    assert q.scale == 127.0 and q.data.tolist() == [[127, -127]]
+    q = L.quantize(np.array([[2.0, 0.0]]), 4)  # :38-41
+    assert q.scale == 3.5 and q.data.tolist() == [[7, 0]]
+    q = L.quantize(np.zeros((2, 2)), 8)  # :44-47
+    assert q.scale == 1.0 and not q.data.any()
+    with pytest.raises(L.ParameterError):
+        L.quantize(np.array([[1.0, np.nan]]), 8)  # :60-62
+    with pytest.raises(L.ParameterError):
+        L.quantize(np.ones((2, 2)), 25)
+
+
+def test_scale_round_clip_half_to_even(L):
+    from paper_2405_16917_b200 import kernels
+
+    halves = np.array([[0.5, 1.5, 2.5, -0.5, -1.5, -2.5]])  # test_backends.py:46-51
+    assert kernels.scale_round_clip(halves, 1.0, 127).tolist() == [[0, 2, 2, 0, -2, -2]]
+    a = O.generate(29, 17, "uniform", 4) * 2.0 - 1.0
+    assert np.array_equal(kernels.scale_round_clip(a, 127.0, 127), O.scale_round_clip(a, 127.0, 127))
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4, 5, 8, 12, 16, 24])
+@pytest.mark.parametrize("shape", [(33, 47), (1, 300), (257, 5)])
+def test_quantize_bit_exact(L, bits, shape):
+    x = O.generate(*shape, "normal", 100 + bits)
+    q = L.quantize(x, bits)
+    d, s = O.quantize_tensor(x, bits)
+    assert q.scale == s
+    assert np.array_equal(q.data, d)
+
+
+def test_quantize_fp32_input_bit_exact(L):
+    x = O.synth(64, 96, "exp:8", 9, 0, 0)  # float32
+    q = L.quantize(x, 8)
+    d, s = O.quantize_tensor(x, 8)
+    assert q.scale == s and np.array_equal(q.data, d)
+
+
+@pytest.mark.parametrize("gran", ["row", "col"])
+@pytest.mark.parametrize("transpose", [False, True])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_quantize_granularity_layouts(N, gran, transpose, dtype):
+    from paper_2405_16917_b200.quant import quantize_device
+
+    x = O.generate(77, 45, "normal", 5).astype(dtype)
+    x[3] = 0.0
+    x[:, 7] = 0.0
+    t = torch.from_numpy(x).to(dev())
+    code = N.GRAN_ROW if gran == "row" else N.GRAN_COL
+    q, s, flag = quantize_device(t, 6, code, transpose, N.I8)
+    d, sref = (O.quantize_rows if gran == "row" else O.quantize_cols)(x, 6)
+    got = q.cpu().numpy().astype(np.int32)
+    if transpose:
+        got = got[:, :77].T
+    else:
+        got = got[:, :45]
+    assert np.array_equal(got, d)
+    assert np.array_equal(s.cpu().numpy(), sref)
+    assert int(flag.item()) == 0
+    # padding columns are zero
+    pad = q.cpu().numpy()[:, (77 if transpose else 45):]
+    assert not pad.any()
+
+
+# ------------------------------------------------------------------ integer GEMM
+
+
+@pytest.mark.parametrize("mnk", [(19, 11, 31), (128, 128, 128), (300, 272, 4096), (1, 16, 8), (513, 129, 1000)])
+def test_imatmul_exact(mnk):
+    from paper_2405_16917_b200 import kernels
+
+    m, n, k = mnk
+    rng = np.random.Generator(np.random.Philox(key=3))
+    a = rng.integers(-127, 128, size=(m, k)).astype(np.int32)
+    b = rng.integers(-127, 128, size=(k, n)).astype(np.int32)
+    out = kernels.imatmul(a, b)
+    assert out.dtype == np.int64
+    assert np.array_equal(out, a.astype(np.int64) @ b.astype(np.int64))
+
+
+def test_imatmul_extremes_and_shape_error():
+    from paper_2405_16917_b200 import kernels
+
+    a = np.full((130, 2048), -127, dtype=np.int32)
+    b = np.full((2048, 40), 127, dtype=np.int32)
+    assert np.all(kernels.imatmul(a, b) == -127 * 127 * 2048)
+    with pytest.raises(ValueError, match="inner dimensions differ"):
+        kernels.imatmul(a, a)
+
+
+@pytest.mark.parametrize("split", [2, 5])
+def test_igemm_split_k_exact(N, split):
+    from paper_2405_16917_b200.quant import quantize_device
+
+    m, n, k = 200, 96, 3000
+    rng = np.random.default_rng(7)
+    a = rng.integers(-127, 128, size=(m, k)).astype(np.int8)
+    bt = rng.integers(-127, 128, size=(n, k)).astype(np.int8)
+    lda = ((k + 15) // 16) * 16
+    ta = torch.zeros((m, lda), dtype=torch.int8, device=dev())
+    tb = torch.zeros((n, lda), dtype=torch.int8, device=dev())
+    ta[:, :k] = torch.from_numpy(a).to(dev())
+    tb[:, :k] = torch.from_numpy(bt).to(dev())
+    out = torch.zeros((m, n), dtype=torch.int32, device=dev())
+    e = N.Epilogue()
+    e.out_dtype, e.accumulate, e.out, e.ldo = N.I32, 1, out.data_ptr(), n
+    rc = N.LIB.lramm_igemm(m, n, k, ctypes.c_void_p(ta.data_ptr()), lda, ctypes.c_void_p(tb.data_ptr()), lda,
+                           ctypes.byref(e), split, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    N.check(rc)
+    ref = a.astype(np.int64) @ bt.astype(np.int64).T
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("bits", [(8, 8), (4, 8), (6, 6), (2, 3)])
+def test_qgemm_bitwise(L, bits):
+    a = O.generate(21, 35, "uniform", 80 + bits[0])
+    b = O.generate(35, 17, "normal", 90 + bits[1])
+    assert np.array_equal(L.qgemm(a, b, *bits), O.qgemm(a, b, *bits))
+
+
+def test_qgemm_alpha_beta_bitwise(L):
+    a = O.generate(6, 5, "uniform", 83)
+    b = O.generate(5, 7, "uniform", 84)
+    c = O.generate(6, 7, "normal", 85)
+    assert np.array_equal(L.qgemm(a, b, 8, 8, alpha=2.0, beta=3.0, c=c), O.qgemm(a, b, 8, 8, 2.0, 3.0, c))
+    assert np.array_equal(L.qgemm(a, b, 8, 8, alpha=-0.5), O.qgemm(a, b, 8, 8, -0.5))
+
+
+def test_qgemm_large_bitwise(L):
+    a = O.generate(700, 1100, "normal", 1)
+    b = O.generate(1100, 333, "normal", 2)
+    assert np.array_equal(L.qgemm(a, b, 8, 8), O.qgemm(a, b, 8, 8))
+
+
+def test_qgemm_errors(L):
+    with pytest.raises(L.ShapeError):
+        L.qgemm(np.ones((2, 3)), np.ones((2, 3)), 8, 8)
+    with pytest.raises(L.OverflowRiskError):
+        L.qgemm(np.ones((1, (1 << 17) + 1)), np.ones(((1 << 17) + 1, 1)), 24, 24)
+    with pytest.raises(L.UnsupportedError):
+        L.qgemm(np.ones((2, 3)), np.ones((3, 2)), 16, 16)
+
+
+def test_integer_matmul_and_dequantize(L):
+    a = O.generate(8, 8, "normal", 71)
+    b = O.generate(8, 8, "normal", 72)
+    qa, qb = L.quantize(a, 8), L.quantize(b, 8)
+    out = L.integer_matmul(qa, qb)
+    assert out.dtype == np.int64
+    assert np.array_equal(out, O.imatmul(*[O.quantize_tensor(x, 8)[0] for x in (a, b)]))
+    d = L.dequantize(qa)
+    assert np.array_equal(d, O.dequantize(*O.quantize_tensor(a, 8)))
+
+
+# ------------------------------------------------------------------ fp64 building blocks
+
+
+@pytest.mark.parametrize("mkn", [(37, 23, 41), (300, 700, 129), (4096, 64, 80)])
+def test_dgemm_matches_blas(mkn):
+    from paper_2405_16917_b200 import kernels
+
+    m, k, n = mkn
+    a = O.generate(m, k, "normal", 1)
+    b = O.generate(k, n, "normal", 2)
+    got = kernels.matmul(a, b)
+    ref = a @ b
+    assert np.max(np.abs(got - ref)) <= 1e-12 * (np.max(np.abs(ref)) + 1.0) * np.sqrt(k)
+
+
+def test_dgemm_transposed_split_k(N):
+    from paper_2405_16917_b200.rsvd import _dgemm
+
+    a = O.generate(5000, 70, "normal", 3)
+    b = O.generate(5000, 90, "normal", 4)
+    got = _dgemm(1, torch.from_numpy(a).to(dev()), torch.from_numpy(b).to(dev()), 70, 90, 5000).cpu().numpy()
+    ref = a.T @ b
+    assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref)) * 10
+    got2 = _dgemm(1, torch.from_numpy(a).to(dev()), torch.from_numpy(b).to(dev()), 70, 90, 5000).cpu().numpy()
+    assert np.array_equal(got, got2)  # deterministic split-K
+
+
+@pytest.mark.parametrize("mw", [(200, 16), (4096, 272), (1000, 74), (333, 100)])
+def test_qr_orthonormal_and_spans(mw):
+    from paper_2405_16917_b200.rsvd import _qr_device
+
+    m, w = mw
+    y = O.synth(m, w, "exp:40", 5, 0, 0).astype(np.float64) @ np.diag(np.linspace(1, 3, w))
+    q = _qr_device(torch.from_numpy(y).to(dev())).cpu().numpy()
+    assert np.linalg.norm(q.T @ q - np.eye(w)) <= 1e-12 * np.sqrt(w)
+    qh = np.linalg.qr(y)[0]
+    # same column-nested basis as Householder up to column signs
+    sign = np.sign(np.sum(q * qh, axis=0))
+    assert np.max(np.abs(q * sign - qh)) <= 1e-10
+
+
+def test_qr_rank_deficient_falls_back_to_householder():
+    from paper_2405_16917_b200.rsvd import _qr_device
+
+    u = np.zeros((30, 1))
+    u[4, 0] = 1.0
+    y = u @ np.ones((1, 11))  # rank 1, width 11 (test_rsvd.py:68-76 shape)
+    q = _qr_device(torch.from_numpy(y).to(dev())).cpu().numpy()
+    assert np.linalg.norm(q.T @ q - np.eye(11)) <= 1e-10
+    assert np.linalg.norm(y - q @ (q.T @ y)) <= 1e-12
+
+
+@pytest.mark.parametrize("shape", [(20, 20), (35, 14), (14, 35), (300, 74), (4096, 272), (1000, 138), (90, 520)])
+def test_svd_contracts(shape):
+    from paper_2405_16917_b200 import kernels
+
+    a = O.generate(*shape, "normal", 5)
+    u, s, v = kernels.svd(a)
+    t = min(shape)
+    sref = np.linalg.svd(a, compute_uv=False)
+    assert u.shape == (shape[0], t) and v.shape == (shape[1], t)
+    assert np.all(np.diff(s) <= 1e-12 * s[0])
+    assert np.max(np.abs(s - sref)) <= 1e-10 * sref[0]
+    assert np.linalg.norm(u.T @ u - np.eye(t)) <= 1e-8 * np.sqrt(t)
+    assert np.linalg.norm(v.T @ v - np.eye(t)) <= 1e-8 * np.sqrt(t)
+    assert np.linalg.norm(a - (u * s) @ v.T) <= 1e-10 * np.linalg.norm(a)
+
+
+def test_svd_matches_reference_jacobi_golden():
+    import os
+
+    from paper_2405_16917_b200 import kernels
+
+    G = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz"))
+    for shape in ((20, 20), (35, 14), (14, 35)):
+        a = O.generate(*shape, "normal", 5)
+        u, s, v = kernels.svd(a)
+        key = f"jac_{shape[0]}x{shape[1]}"
+        assert np.max(np.abs(s - G[key + "_s"])) <= 1e-12 * s[0]
+        sign = np.sign(np.sum(u * G[key + "_u"], axis=0))
+        assert np.max(np.abs(u * sign - G[key + "_u"])) <= 1e-9
+        assert np.max(np.abs(v * sign - G[key + "_v"])) <= 1e-9
+
+
+def test_svd_rank_deficient_completion():
+    from paper_2405_16917_b200 import kernels
+
+    a = O.generate(40, 12, "lowrank", 3, rank=3)
+    u, s, v = kernels.svd(a)
+    assert np.linalg.norm(u.T @ u - np.eye(12)) <= 1e-8
+    assert np.linalg.norm(v.T @ v - np.eye(12)) <= 1e-8
+    assert np.linalg.norm(a - (u * s) @ v.T) <= 1e-10 * np.linalg.norm(a)
