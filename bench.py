@@ -1,0 +1,389 @@
+"""Benchmark of the LRAMM approximate-GEMM hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+One step = one approximate GEMM D ~= A.B through the whole pipeline (randomised SVD of
+both operands with int8 per-row sketch / power / projection GEMMs, fp64 CholeskyQR2 +
+one-sided Jacobi, the three quantised recombination GEMMs) on BASELINE configs[1]
+(m = n = k = 4096, r = 256, p = 16, q = 1, bits (8, 8, 8)).
+
+`value`  = effective approx-GEMM TOPS = 2 m n k * steps * world / (max-over-ranks device
+           time), inputs resident in HBM, each step replayed from one captured CUDA graph;
+`e2e`    = the same metric through the drop-in public API `lramm(numpy A, numpy B, params)`,
+           which calls the C-ABI host entry `lramm_host_lramm`: host->device copies of A, B
+           (pinned) and Omega, the pipeline, and the device->host copy of D every step.
+N > 1 ranks run independent pairs (one per rank, weak scaling, no data-path collective).
+`--impl reference` times the unmodified reference `lramm.lramm()` (installed into
+oracle/_ref) on the host cores on the same config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[1]
+    "c2": dict(m=4096, k=4096, n=4096, rank=256, oversample=16, power_iters=1, bits=(8, 8, 8), tau=128.0,
+               mode="fast", sketch_bits=8, power_bits=8, proj_bits=8, granularity="row"),
+    # BASELINE.json configs[0] (the reference's CPU-runnable case), for quick runs
+    "c1": dict(m=1024, k=1024, n=1024, rank=64, oversample=10, power_iters=1, bits=(8, 8, 8), tau=32.0,
+               mode="fast", sketch_bits=8, power_bits=8, proj_bits=8, granularity="row"),
+}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def synth_pair(cfg, seed, device):
+    """A = U diag(sigma) V^T, B likewise; Haar U, V (QR of seeded Gaussians, sign-fixed);
+    sigma_i = exp(-i/tau) + 1e-4; stored fp32."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(0x1A3A * 1000 + seed)
+
+    def haar(n):
+        z = torch.randn(n, n, generator=g, device=device, dtype=torch.float64)
+        q, r = torch.linalg.qr(z)
+        return q * torch.sign(torch.diagonal(r))
+
+    def mat(rows, cols):
+        t = min(rows, cols)
+        i = torch.arange(1, t + 1, device=device, dtype=torch.float64)
+        sig = torch.exp(-i / cfg["tau"]) + 1e-4
+        u = haar(rows)[:, :t]
+        v = haar(cols)[:, :t]
+        return ((u * sig) @ v.T).to(torch.float32).contiguous()
+
+    return mat(cfg["m"], cfg["k"]), mat(cfg["k"], cfg["n"])
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------ roofline of the dominant kernel
+
+def roofline_probe(L, ta, tb, params, reps=5):
+    """Time the hot path's kernels live (torch profiler over one step), pick the dominant one and
+    express it against its roofline."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(reps):
+            L.lramm_device(ta, tb, params)
+        torch.cuda.synchronize()
+    per = {}
+    launches = 0
+    for ev in prof.events():
+        if ev.device_type.name != "CUDA":
+            continue
+        name = ev.name
+        if "Memcpy" in name or "Memset" in name or "memcpy" in name or "memset" in name:
+            continue
+        launches += 1
+        d = per.setdefault(name, [0.0, 0])
+        d[0] += ev.device_time
+        d[1] += 1
+    total = sum(v[0] for v in per.values())
+    top = max(per.items(), key=lambda kv: kv[1][0])
+    return top[0], top[1][0] / top[1][1], top[1][1] // reps, total / reps, launches // reps, per
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, cfg, world, rank)
+    return run_ours(args, cfg, world, rank, local)
+
+
+def effective_ops(cfg):
+    return 2.0 * cfg["m"] * cfg["n"] * cfg["k"]
+
+
+def workload_config(cfg, args, world):
+    return {"workload": f"BASELINE configs[1]: {cfg['m']}x{cfg['k']}x{cfg['n']} fp32 exp:{int(cfg['tau'])} spectrum, "
+                        f"r={cfg['rank']} p={cfg['oversample']} q={cfg['power_iters']}, int8 per-row sketch/power/"
+                        f"projection GEMMs, recombination bits {cfg['bits']}",
+            "name": args.config, "m": cfg["m"], "k": cfg["k"], "n": cfg["n"], "rank": cfg["rank"],
+            "oversample": cfg["oversample"], "power_iters": cfg["power_iters"], "bits": list(cfg["bits"]),
+            "mode": cfg["mode"], "granularity": cfg["granularity"], "pairs_per_rank": 1,
+            "parallelism": f"{world} independent pair(s), one per rank" if world > 1 else "single GPU",
+            "l2": "inputs (2 x 64 MiB fp32) exceed the 126 MB L2; no explicit flush"}
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
+    try:
+        import lramm as ref  # the unmodified reference package
+    except Exception as exc:  # pragma: no cover
+        print(json.dumps({"impl": "reference", "unavailable": f"reference not importable: {exc}"}))
+        return 0
+    import torch
+
+    a, b = synth_pair(cfg, 0, torch.device("cpu"))
+    a, b = a.numpy(), b.numpy()
+    params = ref.LrammParams(rank=cfg["rank"], bits=tuple(cfg["bits"]), power_iters=cfg["power_iters"],
+                             oversample=cfg["oversample"], seed=0)
+    steps = max(1, min(args.steps, 2))
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        ref.lramm(a, b, params)
+        times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    value = effective_ops(cfg) / t / 1e12
+    cores = os.cpu_count()
+    line = {"metric": "effective approx-GEMM TOPS (2mnk/time)", "value": value, "unit": "TOPS", "n_gpus": args.gpus,
+            "steps": steps, "warmup": 0, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64 (fp32 inputs upcast), int64 QM products", "data": "synthetic",
+            "impl": "reference", "config": workload_config(cfg, args, 1),
+            "cpu_baseline": {"value": value, "unit": "TOPS", "cores": cores, "kind": "reference",
+                             "sample": f"{steps} full reference lramm() call(s) on the same config "
+                                       f"(backend {ref.backend_name()}, warm-up skipped; steps capped at 2 "
+                                       f"so the run stays within minutes)"},
+            "e2e": {"value": value, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args, cfg, world, rank, local):
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2405_16917_b200 as L
+
+    a, b = synth_pair(cfg, rank, dev)
+    params = L.LrammParams(rank=cfg["rank"], bits=tuple(cfg["bits"]), power_iters=cfg["power_iters"],
+                           oversample=cfg["oversample"], seed=rank, mode=cfg["mode"], sketch_bits=cfg["sketch_bits"],
+                           power_bits=cfg["power_bits"], proj_bits=cfg["proj_bits"], granularity=cfg["granularity"],
+                           out_dtype=np.float32)
+    # warm-up (also sets kernel attributes before capture)
+    for _ in range(max(1, args.warmup)):
+        out, status, _t = L.lramm_device(a, b, params)
+    torch.cuda.synchronize()
+    st = int(status.item())
+    if st:
+        raise RuntimeError(f"lramm status {st}")
+    # capture one step into a CUDA graph
+    stream = torch.cuda.Stream(device=dev)
+    stream.wait_stream(torch.cuda.current_stream(dev))
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        L.lramm_device(a, b, params, out=out)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=stream):
+            L.lramm_device(a, b, params, out=out)
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    ms_per_step = ms / args.steps
+    value = effective_ops(cfg) * world / (ms_per_step * 1e-3) / 1e12
+
+    # ---- e2e through the drop-in public API (host buffers, C-ABI host entry point)
+    ha = torch.empty(a.shape, dtype=torch.float32, pin_memory=True)
+    hb = torch.empty(b.shape, dtype=torch.float32, pin_memory=True)
+    ha.copy_(a.cpu())
+    hb.copy_(b.cpu())
+    na, nb = ha.numpy(), hb.numpy()
+    p64 = L.LrammParams(rank=cfg["rank"], bits=tuple(cfg["bits"]), power_iters=cfg["power_iters"],
+                        oversample=cfg["oversample"], seed=rank, mode=cfg["mode"], sketch_bits=cfg["sketch_bits"],
+                        power_bits=cfg["power_bits"], proj_bits=cfg["proj_bits"], granularity=cfg["granularity"])
+    hout = torch.empty((cfg["m"], cfg["n"]), dtype=torch.float64, pin_memory=True).numpy()
+    for _ in range(max(1, min(args.warmup, 2))):
+        L.lramm(na, nb, p64, out=hout)
+    e2e_steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        d, _ = L.lramm(na, nb, p64, out=hout)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    wa = min(cfg["rank"] + cfg["oversample"], cfg["k"])
+    h2d = 4 * (cfg["m"] * cfg["k"] + cfg["k"] * cfg["n"]) + 8 * (cfg["k"] * wa + cfg["n"] * wa)
+    d2h = 8 * cfg["m"] * cfg["n"]
+    e2e = {"value": effective_ops(cfg) * world / e2e_s / 1e12, "unit": "TOPS", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+           "path": "lramm(numpy) -> lramm_host_lramm (C ABI), pinned A/B/D, fp64 D like the reference"}
+
+    # ---- dominant kernel + launches (live, torch profiler over device-resident steps)
+    top_name, top_us, top_per_step, step_us, launches, per = roofline_probe(L, a, b, params)
+    peaks = measured_peaks()
+    roof = dominant_roofline(top_name, top_us, cfg, peaks)
+    roof["kernel"] = top_name
+    roof["us_per_launch"] = top_us
+    roof["launches_per_step"] = top_per_step
+    roof["share_of_step"] = top_us * top_per_step / step_us if step_us else None
+
+    line = {"metric": "effective approx-GEMM TOPS (2mnk/time)", "value": value, "unit": "TOPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "int8 x int8 -> int32 (tcgen05) sketch/QM GEMMs; fp64 factorisation; fp32 D",
+            "data": "synthetic (SURVEY §8(d) spectrum, Haar factors from seeded torch QR)",
+            "config": workload_config(cfg, args, world), "clocks": clocks.summary(), "e2e": e2e,
+            "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches, "roofline": roof}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, a, b)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def dominant_roofline(name, us, cfg, peaks):
+    """Algorithmic work of the dominant kernel per launch over its measured time."""
+    m, k, n, r = cfg["m"], cfg["k"], cfg["n"], cfg["rank"]
+    w = r + cfg["oversample"]
+    fp64_peak = 36.7  # TFLOP/s, DFMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak.txt)
+    if "jacobi" in name:
+        # one-sided Jacobi on w x w: ~ sweeps * w(w-1)/2 pairs * 6w flops; sweeps measured ~11
+        flops = 11 * (w * (w - 1) / 2) * 6 * w
+        achieved = flops / (us * 1e-6) / 1e12
+        return {"bound": "tensor", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak, "traffic": None,
+                "peak_source": "measured fp64 DFMA peak (not in MEASURED_PEAKS.json); kernel is latency-bound"}
+    if "chol" in name or "trinv" in name:
+        flops = w ** 3 / 3.0
+        achieved = flops / (us * 1e-6) / 1e12
+        return {"bound": "tensor", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak, "traffic": None,
+                "peak_source": "measured fp64 DFMA peak; kernel is latency-bound"}
+    if "dgemm" in name:
+        flops = 2.0 * m * w * w
+        achieved = flops / (us * 1e-6) / 1e12
+        return {"bound": "tensor", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak, "traffic": None, "peak_source": "measured fp64 DFMA peak"}
+    # int8 tcgen05 GEMM / quantiser: HBM-bound at these shapes
+    hbm = peaks.get("hbm_gbs", 6538.0)
+    byts = m * k * 1 + w * k * 1 + m * w * 8
+    achieved = byts / (us * 1e-6) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+
+
+def cpu_baseline(cfg, a, b):
+    """The unmodified reference (oracle/_ref) timed on this host on a bounded sample."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
+        import lramm as ref
+    except Exception as exc:
+        return {"value": None, "unit": "TOPS", "cores": os.cpu_count(), "kind": "reference",
+                "sample": f"unavailable: {exc}"}
+    ha, hb = a.cpu().numpy(), b.cpu().numpy()
+    params = ref.LrammParams(rank=cfg["rank"], bits=tuple(cfg["bits"]), power_iters=cfg["power_iters"],
+                             oversample=cfg["oversample"], seed=0)
+    t0 = time.perf_counter()
+    ref.lramm(ha, hb, params)
+    t = time.perf_counter() - t0
+    return {"value": effective_ops(cfg) / t / 1e12, "unit": "TOPS", "cores": os.cpu_count(), "kind": "reference",
+            "sample": f"one full reference lramm() call on the same {cfg['m']}x{cfg['k']}x{cfg['n']} inputs "
+                      f"({t:.1f} s, backend {ref.backend_name()}, OpenBLAS threads = host cores)"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

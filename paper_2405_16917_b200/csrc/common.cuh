@@ -39,6 +39,18 @@ inline int bit_cap(int bits) { return (1 << (bits - 1)) - 1; }  // quant.py:20-2
 
 int num_sms();
 
+// opt a kernel into the largest dynamic shared memory the device allows next to its static smem
+template <class K>
+inline cudaError_t allow_max_dyn_smem(K kernel) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, kernel);
+  if (e != cudaSuccess) return e;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+}
+
 // Bump allocator over a caller-provided workspace (256-byte aligned slices).
 struct Arena {
   char *base = nullptr;

@@ -223,11 +223,12 @@ def lramm_device(a: torch.Tensor, b: torch.Tensor, params: LrammParams, c: torch
     return out, status, t
 
 
-def lramm(a, b, params, c=None):
+def lramm(a, b, params, c=None, out=None):
     """Approximate alpha * A @ B + beta * C through the three-stage pipeline (pipeline.py:159-214).
 
     Returns (D, StageTimings).  Deterministic: identical inputs and params give a
-    bitwise identical D.
+    bitwise identical D.  Extension: ``out`` (C-contiguous, m x n, params.out_dtype)
+    receives D, e.g. a pinned host buffer.
     """
     m, k, n = _validate(a, b, params, c)
     d1, d2, d3 = params.bits
@@ -236,7 +237,7 @@ def lramm(a, b, params, c=None):
         ta = to_device_matrix(a, dev)
         tb = to_device_matrix(b, dev)
         tc = to_device_matrix(c, dev) if c is not None else None
-        out, status, t = lramm_device(ta, tb, params, tc, timings=True)
+        out, status, t = lramm_device(ta, tb, params, tc, out=out, timings=True)
         st = int(status.item())
         if st:
             N.check(st)
@@ -257,7 +258,12 @@ def lramm(a, b, params, c=None):
     om_a = OMEGA.host_omega(seed_a, k, wa)
     om_b = OMEGA.host_omega(seed_b, n, wb)
     out_dt = np.dtype(params.out_dtype)
-    d = np.empty((m, n), dtype=out_dt)
+    if out is not None:
+        if out.shape != (m, n) or out.dtype != out_dt or not out.flags["C_CONTIGUOUS"]:
+            raise ShapeError(f"out must be a C-contiguous {(m, n)} {out_dt} array")
+        d = out
+    else:
+        d = np.empty((m, n), dtype=out_dt)
     p = _params(params)
     t = N.Timings()
     vp = lambda x: ctypes.c_void_p(x.ctypes.data) if x is not None else ctypes.c_void_p(0)  # noqa: E731

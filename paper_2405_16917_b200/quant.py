@@ -114,10 +114,13 @@ def quantize(a, bits):
 
 def dequantize(q):
     """Map integers back to float64: entries / scale (quant.py:74-76)."""
+    # elementwise true division by a broadcast tensor (a python-scalar divisor is
+    # turned into a reciprocal multiply by torch, which is not the reference's rounding)
     if _is_cuda(q.data):
-        return q.data.to(torch.float64) / q.scale
+        return q.data.to(torch.float64) / torch.full((1, 1), q.scale, dtype=torch.float64, device=q.data.device)
     dev = require_device()
-    return (torch.from_numpy(np.ascontiguousarray(q.data)).to(dev).to(torch.float64) / q.scale).cpu().numpy()
+    d = torch.from_numpy(np.ascontiguousarray(q.data)).to(dev).to(torch.float64)
+    return (d / torch.full((1, 1), q.scale, dtype=torch.float64, device=dev)).cpu().numpy()
 
 
 def _check_overflow(k, bits_a, bits_b):
