@@ -2,109 +2,121 @@
 // matrices, triangular multiplies, the lift U = Q.u, and (parity mode) the
 // sketch / power / projection products of the reference (rsvd.py:57-77).
 //
-// 64x64 output tile per 256-thread CTA, 4x4 outputs per thread (strided so a
-// warp's shared-memory reads are conflict-free), K staged 16 at a time through
-// double-buffered shared memory.  trans_a = 1 evaluates A^T.B for tall row-major
-// operands (A: K x M) with split-K over the long dimension and a fixed-order
-// reduction, so results are bitwise reproducible run to run.
+// FP64 tensor pipe (mma.sync.m8n8k4.f64, "DMMA": same 37 TFLOP/s peak as DFMA on
+// B200 but 8x fewer issued instructions).  64 x 64 CTA tile, 8 warps each owning
+// a 32 x 16 sub-tile (4 x 2 DMMA tiles), K staged 32 at a time through double-
+// buffered shared memory with cp.async.  trans_a = 1 evaluates A^T.B for tall
+// row-major operands (A: K x M) with split-K over the long dimension and a
+// fixed-order reduction, so results are bitwise reproducible run to run.
 #include <algorithm>
+#include <mutex>
 
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace lramm {
 namespace {
 
-constexpr int TM = 64, TN = 64, TK = 16;
+constexpr int TM = 64, TN = 64, TK = 32;
+constexpr int LDA = TK + 4;  // As[m][k] (NN) row stride
+constexpr int LDT = TM + 4;  // As[k][m] (TN) and Bs[k][n] row stride
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
 
 template <bool TRANS_A>
 __global__ void __launch_bounds__(256) dgemm_kernel(int64_t M, int64_t N, int64_t K, const double *__restrict__ A,
                                                     int64_t lda, const double *__restrict__ B, int64_t ldb,
                                                     double *__restrict__ C, int64_t ldc, int64_t k_per_split,
                                                     int64_t split_stride) {
-  __shared__ double As[2][TK][TM + 1];
-  __shared__ double Bs[2][TK][TN + 1];
-  const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
+  constexpr int ASZ = TRANS_A ? TK * LDT : TM * LDA;
+  extern __shared__ __align__(16) double dg_smem[];
+  double(*As)[ASZ] = reinterpret_cast<double(*)[ASZ]>(dg_smem);
+  double(*Bs)[TK * LDT] = reinterpret_cast<double(*)[TK * LDT]>(dg_smem + 2 * ASZ);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;  // warp tile: rows wm*32.., cols wn*16..
   const int64_t m0 = (int64_t)blockIdx.x * TM, n0 = (int64_t)blockIdx.y * TN;
   const int64_t kbeg = (int64_t)blockIdx.z * k_per_split;
   const int64_t kend = min(K, kbeg + k_per_split);
-  double acc[4][4];
+  double acc[4][2][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  double ra[4], rb[4];
-  auto load_regs = [&](int64_t k0) {
-#pragma unroll
-    for (int l = 0; l < 4; ++l) {
-      int e = tid + l * 256;  // 0..1023 = TK x 64
-      int kk, mm;
-      if (TRANS_A) {  // A is K x M: coalesced along m
-        kk = e >> 6;
-        mm = e & 63;
-        int64_t gk = k0 + kk, gm = m0 + mm;
-        ra[l] = (gk < kend && gm < M) ? A[gk * lda + gm] : 0.0;
-      } else {  // A is M x K: 16 consecutive k per row
-        mm = e >> 4;
-        kk = e & 15;
-        int64_t gk = k0 + kk, gm = m0 + mm;
-        ra[l] = (gk < kend && gm < M) ? A[gm * lda + gk] : 0.0;
+  auto stage = [&](int buf, int64_t k0) {
+    // A
+    if (TRANS_A) {  // A is K x M: rows k, contiguous m
+      for (int e = tid; e < TK * TM; e += 256) {
+        const int kk = e >> 6, mm = e & 63;
+        const int64_t gk = k0 + kk, gm = m0 + mm;
+        const bool v = gk < kend && gm < M;
+        sm100::cp_async8(&As[buf][kk * LDT + mm], A + (v ? gk * lda + gm : 0), v);
       }
-      int bk = e >> 6, bn = e & 63;
-      int64_t gk = k0 + bk, gn = n0 + bn;
-      rb[l] = (gk < kend && gn < N) ? B[gk * ldb + gn] : 0.0;
+    } else {  // A is M x K: rows m, contiguous k
+      for (int e = tid; e < TM * TK; e += 256) {
+        const int mm = e >> 5, kk = e & 31;
+        const int64_t gk = k0 + kk, gm = m0 + mm;
+        const bool v = gk < kend && gm < M;
+        sm100::cp_async8(&As[buf][mm * LDA + kk], A + (v ? gm * lda + gk : 0), v);
+      }
     }
-  };
-  auto store_regs = [&](int buf) {
-#pragma unroll
-    for (int l = 0; l < 4; ++l) {
-      int e = tid + l * 256;
-      if (TRANS_A)
-        As[buf][e >> 6][e & 63] = ra[l];
-      else
-        As[buf][e & 15][e >> 4] = ra[l];
-      Bs[buf][e >> 6][e & 63] = rb[l];
+    for (int e = tid; e < TK * TN; e += 256) {
+      const int kk = e >> 6, nn = e & 63;
+      const int64_t gk = k0 + kk, gn = n0 + nn;
+      const bool v = gk < kend && gn < N;
+      sm100::cp_async8(&Bs[buf][kk * LDT + nn], B + (v ? gk * ldb + gn : 0), v);
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
   int buf = 0;
-  if (kbeg < kend) {
-    load_regs(kbeg);
-    store_regs(0);
-  }
-  __syncthreads();
+  if (kbeg < kend) stage(0, kbeg);
   for (int64_t k0 = kbeg; k0 < kend; k0 += TK) {
     const bool more = k0 + TK < kend;
-    if (more) load_regs(k0 + TK);
+    if (more) {
+      stage(buf ^ 1, k0 + TK);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double *as = As[buf];
+    const double *bs = Bs[buf];
 #pragma unroll
-    for (int kk = 0; kk < TK; ++kk) {
-      double a[4], b[4];
+    for (int kk = 0; kk < TK; kk += 4) {
+      double a[4], b[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[buf][kk][ty + 16 * i];
+      for (int i = 0; i < 4; ++i) {
+        const int m = wm * 32 + i * 8 + g;
+        a[i] = TRANS_A ? as[(kk + t4) * LDT + m] : as[m * LDA + kk + t4];
+      }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[buf][kk][tx + 16 * j];
+      for (int j = 0; j < 2; ++j) b[j] = bs[(kk + t4) * LDT + wn * 16 + j * 8 + g];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 2; ++j) dmma(acc[i][j], a[i], b[j]);
     }
-    if (more) {
-      store_regs(buf ^ 1);
-      __syncthreads();
-      buf ^= 1;
-    }
+    __syncthreads();
+    buf ^= 1;
   }
   double *Cz = C + (int64_t)blockIdx.z * split_stride;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    int64_t r = m0 + ty + 16 * i;
+    const int64_t r = m0 + wm * 32 + i * 8 + g;
     if (r >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int64_t c = n0 + tx + 16 * j;
-      if (c < N) Cz[r * ldc + c] = acc[i][j];
-    }
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t c = n0 + wn * 16 + j * 8 + 2 * t4 + h;
+        if (c < N) Cz[r * ldc + c] = acc[i][j][h];
+      }
   }
 }
 
@@ -121,11 +133,11 @@ __global__ void splitk_reduce_kernel(const double *__restrict__ parts, int split
 }
 
 int choose_splits(int trans_a, int64_t M, int64_t N, int64_t K) {
-  if (!trans_a) return 1;
   int64_t tiles = ceil_div(M, TM) * ceil_div(N, TN);
   int64_t want = ceil_div(2LL * num_sms(), tiles);
   int64_t max_by_k = std::max<int64_t>(1, K / 256);
-  return (int)std::max<int64_t>(1, std::min<int64_t>(want, std::min<int64_t>(max_by_k, 64)));
+  int64_t s = std::max<int64_t>(1, std::min<int64_t>(want, std::min<int64_t>(max_by_k, 64)));
+  return (int)s;
 }
 
 }  // namespace
@@ -145,10 +157,18 @@ int dgemm_device(int trans_a, int64_t M, int64_t N, int64_t K, const double *A, 
   dim3 grid((unsigned)ceil_div(M, TM), (unsigned)ceil_div(N, TN), (unsigned)splits);
   double *out = splits > 1 ? (double *)ws : C;
   int64_t ldo = splits > 1 ? N : ldc;
+  static std::once_flag once;
+  cudaError_t e = cudaSuccess;
+  std::call_once(once, [&] {
+    e = allow_max_dyn_smem(dgemm_kernel<true>);
+    if (e == cudaSuccess) e = allow_max_dyn_smem(dgemm_kernel<false>);
+  });
+  LRAMM_CUDA_TRY(e);
+  const size_t smem_t = (size_t)(2 * TK * LDT + 2 * TK * LDT) * 8, smem_n = (size_t)(2 * TM * LDA + 2 * TK * LDT) * 8;
   if (trans_a)
-    dgemm_kernel<true><<<grid, 256, 0, st>>>(M, N, K, A, lda, B, ldb, out, ldo, kps, M * N);
+    dgemm_kernel<true><<<grid, 256, smem_t, st>>>(M, N, K, A, lda, B, ldb, out, ldo, kps, M * N);
   else
-    dgemm_kernel<false><<<grid, 256, 0, st>>>(M, N, K, A, lda, B, ldb, out, ldo, kps, M * N);
+    dgemm_kernel<false><<<grid, 256, smem_n, st>>>(M, N, K, A, lda, B, ldb, out, ldo, kps, M * N);
   LRAMM_LAUNCH_CHECK();
   if (splits > 1) {
     int g = (int)std::min<int64_t>(ceil_div(M * N, 256), 8LL * num_sms());

@@ -327,6 +327,26 @@ __global__ void gather_info_kernel(const int *a, const int *b, const int *ca, co
   if (nfa[0] || nfb[0]) nonfinite[0] = 1;
 }
 
+// per-thread, per-device side stream + fork/join events
+struct SideStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int dev = -1;
+};
+SideStream &side_stream() {
+  static thread_local SideStream s[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream &x = s[dev & 15];
+  if (x.dev != dev) {
+    cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+    x.dev = dev;
+  }
+  return x;
+}
+
 }  // namespace
 
 size_t rsvd_ws_bytes(int64_t rows, int64_t cols, const lramm_params_t &P, int x_dtype) {
@@ -398,9 +418,15 @@ int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t 
     return LRAMM_OK;
   };
   LRAMM_TRY(mark(0));
-  // ---- rsvd of both operands (pipeline.py:183-186)
+  // ---- rsvd of both operands (pipeline.py:183-186): independent chains, so B runs on a
+  // forked side stream (event fork/join; capturable into a CUDA graph)
+  SideStream &side = side_stream();
+  LRAMM_CUDA_TRY(cudaEventRecord(side.fork, st));
+  LRAMM_CUDA_TRY(cudaStreamWaitEvent(side.st, side.fork, 0));
+  LRAMM_TRY(run_rsvd(b, in_dtype, L.rb, P, omega_b, L.UB, r, L.SB, L.VB, r, side.st));
   LRAMM_TRY(run_rsvd(a, in_dtype, L.ra, P, omega_a, L.UA, r, L.SA, L.VA, r, st));
-  LRAMM_TRY(run_rsvd(b, in_dtype, L.rb, P, omega_b, L.UB, r, L.SB, L.VB, r, st));
+  LRAMM_CUDA_TRY(cudaEventRecord(side.join, side.st));
+  LRAMM_CUDA_TRY(cudaStreamWaitEvent(st, side.join, 0));
   LRAMM_TRY(mark(1));
   // ---- scaling (pipeline.py:188-193): Usc = U_A sigma_A, Zsc^T = V_B sigma_B
   scale_cols_kernel<<<elem_grid(m * r), 256, 0, st>>>(L.UA, m, (int)r, r, L.SA, L.Usc, r);
