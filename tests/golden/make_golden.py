@@ -139,7 +139,9 @@ def main():
         params = lramm.LrammParams(rank=rank, bits=bits, power_iters=q_iters, oversample=p, seed=seed)
         with _pure_backend():
             d_pure, _ = lramm.lramm(a, b, params)
+        d_comp, _ = lramm.lramm(a, b, params)
         out[f"lr_{name}_pure"] = d_pure
+        out[f"lr_{name}_compiled"] = d_comp
 
     # ---- config 1 (BASELINE configs[0]) summary: too large to store whole --------
     a = O.synth(1024, 1024, "exp:32", 1, 0, 0)
