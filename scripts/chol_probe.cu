@@ -20,7 +20,7 @@ int main(int argc, char** argv) {
     cudaMemset(L, 0, w*w*8);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     cudaEventRecord(a);
-    lramm::chol_kernel<<<1, lramm::kCholThreads, lramm::kCholSmem>>>(G, w, w, L, info);
+    lramm::chol_kernel<<<1, lramm::kCholThreads, lramm::kCholSmem>>>(G, w, w, L, info, nullptr);
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
     long long t[4096]; cudaMemcpyFromSymbol(t, lramm_trace, sizeof(t));
