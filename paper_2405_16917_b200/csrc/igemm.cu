@@ -33,6 +33,37 @@ struct EpiDev {
   int64_t ldc;
 };
 
+// Correctly rounded a / s for |a| < 2^53 integer-valued a and normal s > 0, given y = RN(1/s):
+// Markstein step q1 = RN(q0 + r y), r = a - q0 s (exact by FMA), then an exact residual check
+// against the neighbour in the direction of the residual (ties to even).  Bit-identical to
+// IEEE division (__ddiv_rn), ~10 instructions instead of the iterative divide.
+__device__ __forceinline__ double next_toward(double x, bool up) {
+  if (x == 0.0) return up ? __longlong_as_double(1LL) : -__longlong_as_double(1LL);
+  const long long b = __double_as_longlong(x);
+  return __longlong_as_double(((x > 0.0) == up) ? b + 1 : b - 1);
+}
+
+__device__ __forceinline__ double div_exact(double a, double s, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double r0 = __fma_rn(-q0, s, a);
+  const double q1 = __fma_rn(r0, y, q0);
+  const double r1 = __fma_rn(-q1, s, a);
+  // q1 is the correctly rounded quotient iff |r1| <= s ulp(q1) / 2 (strictly < : no tie to resolve)
+  const long long eb = __double_as_longlong(q1) & 0x7FF0000000000000LL;
+  if (eb > (53LL << 52)) {
+    const double half_ulp = __longlong_as_double(eb - (53LL << 52));  // ulp(q1) / 2 for normal q1
+    if (fabs(r1) < __dmul_rn(s, half_ulp)) return q1;
+  } else if (r1 == 0.0) {
+    return q1;
+  }
+  const double qn = next_toward(q1, r1 > 0.0);
+  const double rn = __fma_rn(-qn, s, a);
+  const double e1 = fabs(r1), en = fabs(rn);
+  if (en < e1) return qn;
+  if (en == e1) return (__double_as_longlong(qn) & 1) ? q1 : qn;  // tie: even mantissa
+  return q1;
+}
+
 // reference dequantisation + alpha/beta on one accumulator (bit-exact IEEE fp64)
 __device__ __forceinline__ double epi_value(const EpiDev &e, int32_t acc, int64_t row, int64_t col) {
   double rs = e.row_scale ? e.row_scale[row * e.row_scale_inc] : 1.0;
@@ -45,6 +76,16 @@ __device__ __forceinline__ double epi_value(const EpiDev &e, int32_t acc, int64_
   } else if (e.alpha != 1.0) {
     v = __dmul_rn(e.alpha, v);
   }
+  return v;
+}
+
+__device__ __forceinline__ double epi_alpha_beta(const EpiDev &e, double v, int64_t row, int64_t col) {
+  if (e.beta != 0.0 && e.c != nullptr) {
+    double cv = e.c_dtype == LRAMM_F32 ? (double)((const float *)e.c)[row * e.ldc + col]
+                                       : ((const double *)e.c)[row * e.ldc + col];
+    return __dadd_rn(__dmul_rn(e.alpha, v), __dmul_rn(e.beta, cv));
+  }
+  if (e.alpha != 1.0) return __dmul_rn(e.alpha, v);
   return v;
 }
 
@@ -69,9 +110,13 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 128;  // bytes == int8 elements == one 128-B swizzle row
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 constexpr int kSmemBudget = 200 * 1024;
 
+// epilogue kinds (compile time): raw int32 store / atomic add, or dequantised f32 / f64
+enum { EK_I32 = 0, EK_I32_ATOMIC = 1, EK_F32 = 2, EK_F64 = 3 };
+
+template <int EK, bool TRANS, bool AB>
 __global__ void __launch_bounds__(kThreads, 1)
     igemm_tn_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                     int64_t M, int64_t N, int64_t K, int BN, int stages, int kb_per_split, EpiDev epi) {
@@ -141,29 +186,98 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::mma_commit(tmem_full);
     }
   } else {
-    // epilogue warps 2..5
-    const int quarter = warp & 3;
-    const int64_t row = m0 + quarter * 32 + lane;
+    // epilogue warps 2..9: TMEM -> registers (thread = row; the two warps of a TMEM lane quarter
+    // take alternate 16-column halves) -> dequant -> shared tile (32-column chunks in the drained
+    // pipeline buffers) -> coalesced stores (warp = rows, lanes = columns)
+    constexpr bool RAW = EK == EK_I32 || EK == EK_I32_ATOMIC;
+    const int ew = warp - 2;               // 0..7
+    const int quarter = warp & 3;          // TMEM lane quarter (hardware: warp id mod 4)
+    const int half = ew >> 2;              // column half of each 32-column chunk
+    const int etid = threadIdx.x - 64;     // 0..255
+    const int rloc = quarter * 32 + lane;
+    const int64_t row = m0 + rloc;
     if (nkb > 0) {
       sm100::mbar_wait(tmem_full, 0);
       sm100::tc_fence_after();
     }
-    for (int c0 = 0; c0 < BN; c0 += 16) {
+    double rs = 1.0;
+    if (!RAW && epi.row_scale) rs = epi.row_scale[(row < M ? row : M - 1) * epi.row_scale_inc];
+    const bool tensor_scale = epi.col_scale == nullptr || epi.col_scale_inc == 0;
+    double s_t = 1.0, y_t = 1.0;
+    if (!RAW && tensor_scale) {
+      s_t = __dmul_rn(rs, epi.col_scale ? epi.col_scale[0] : 1.0);
+      y_t = __drcp_rn(s_t);
+    }
+    double *tile = reinterpret_cast<double *>(smem);  // 128 x 33
+    int32_t *itile = reinterpret_cast<int32_t *>(smem);
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      const int cb = c0 + half * 16;
       uint32_t r[16];
-      if (nkb > 0) {
-        sm100::tmem_ld16(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, r);
+      if (nkb > 0 && cb < BN) {
+        sm100::tmem_ld16(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb, r);
         sm100::tmem_wait_ld();
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) r[j] = 0;
       }
-      if (row < M) {
+      if (RAW) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) itile[rloc * 33 + half * 16 + j] = (int32_t)r[j];
+      } else if (tensor_scale) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) tile[rloc * 33 + half * 16 + j] = div_exact((double)(int32_t)r[j], s_t, y_t);
+      } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const int64_t col = n0 + c0 + j;
-          if (col < N) epi_store(epi, (int32_t)r[j], row, col);
+          const int64_t col = min(n0 + cb + j, N - 1);
+          const double s = __dmul_rn(rs, epi.col_scale[col * epi.col_scale_inc]);
+          tile[rloc * 33 + half * 16 + j] = div_exact((double)(int32_t)r[j], s, __drcp_rn(s));
         }
       }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const int nc = min(32, BN - c0);
+      if (!TRANS) {
+        const int64_t gcol = n0 + c0 + lane;
+        const bool colok = lane < nc && gcol < N;
+        for (int rr = etid >> 5; rr < 128; rr += 8) {
+          const int64_t grow = m0 + rr;
+          if (grow < M && colok) {
+            const int64_t idx = grow * epi.ldo + gcol;
+            if constexpr (EK == EK_I32) {
+              ((int32_t *)epi.out)[idx] = itile[rr * 33 + lane];
+            } else if constexpr (EK == EK_I32_ATOMIC) {
+              atomicAdd((int32_t *)epi.out + idx, itile[rr * 33 + lane]);
+            } else {
+              double v = tile[rr * 33 + lane];
+              if constexpr (AB) v = epi_alpha_beta(epi, v, grow, gcol);
+              if constexpr (EK == EK_F64) ((double *)epi.out)[idx] = v;
+              else ((float *)epi.out)[idx] = __double2float_rn(v);
+            }
+          }
+        }
+      } else {
+        // out^T: tile column j is a contiguous output row; lanes run over tile rows
+        for (int jj = etid >> 5; jj < nc; jj += 8) {
+          const int64_t gcol = n0 + c0 + jj;
+          if (gcol >= N) continue;
+          for (int rr = lane; rr < 128; rr += 32) {
+            const int64_t grow = m0 + rr;
+            if (grow >= M) continue;
+            const int64_t idx = gcol * epi.ldo + grow;
+            if constexpr (EK == EK_I32) {
+              ((int32_t *)epi.out)[idx] = itile[rr * 33 + jj];
+            } else if constexpr (EK == EK_I32_ATOMIC) {
+              atomicAdd((int32_t *)epi.out + idx, itile[rr * 33 + jj]);
+            } else {
+              double v = tile[rr * 33 + jj];
+              if constexpr (AB) v = epi_alpha_beta(epi, v, grow, gcol);
+              if constexpr (EK == EK_F64) ((double *)epi.out)[idx] = v;
+              else ((float *)epi.out)[idx] = __double2float_rn(v);
+            }
+          }
+        }
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
     }
   }
   sm100::tc_fence_before();
@@ -256,14 +370,24 @@ int igemm_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, 
   CUtensorMap ta, tb;
   LRAMM_TRY(make_tmap_i8(&ta, a, M, K, lda, BM));
   LRAMM_TRY(make_tmap_i8(&tb, b, N, K, ldb, BN));
-  static std::once_flag attr_once;
-  cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [&] {
-    attr_err = allow_max_dyn_smem(igemm_tn_kernel);
-  });
-  LRAMM_CUDA_TRY(attr_err);
+  const int ek = epi.out_dtype == LRAMM_I32 ? (epi.accumulate ? EK_I32_ATOMIC : EK_I32)
+                                            : (epi.out_dtype == LRAMM_F64 ? EK_F64 : EK_F32);
+  const bool ab = ek >= EK_F32 && (epi.alpha != 1.0 || (epi.beta != 0.0 && epi.c != nullptr));
+  using KernT = void (*)(CUtensorMap, CUtensorMap, int64_t, int64_t, int64_t, int, int, int, EpiDev);
+  KernT kern = nullptr;
+#define LRAMM_IG_PICK(EKV, TR, ABV) \
+  if (ek == EKV && (epi.transpose_out != 0) == TR && ab == ABV) kern = igemm_tn_kernel<EKV, TR, ABV>;
+  LRAMM_IG_PICK(EK_I32, false, false) LRAMM_IG_PICK(EK_I32, true, false)
+  LRAMM_IG_PICK(EK_I32_ATOMIC, false, false) LRAMM_IG_PICK(EK_I32_ATOMIC, true, false)
+  LRAMM_IG_PICK(EK_F32, false, false) LRAMM_IG_PICK(EK_F32, true, false)
+  LRAMM_IG_PICK(EK_F32, false, true) LRAMM_IG_PICK(EK_F32, true, true)
+  LRAMM_IG_PICK(EK_F64, false, false) LRAMM_IG_PICK(EK_F64, true, false)
+  LRAMM_IG_PICK(EK_F64, false, true) LRAMM_IG_PICK(EK_F64, true, true)
+#undef LRAMM_IG_PICK
+  if (!kern) return fail(LRAMM_ERR_PARAM, "igemm: unsupported epilogue");
+  LRAMM_CUDA_TRY(allow_max_dyn_smem(kern));
   dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(N, BN), (unsigned)split_k);
-  igemm_tn_kernel<<<grid, kThreads, smem, st>>>(ta, tb, M, N, K, BN, stages, kb_per, to_dev(epi));
+  kern<<<grid, kThreads, smem, st>>>(ta, tb, M, N, K, BN, stages, kb_per, to_dev(epi));
   LRAMM_LAUNCH_CHECK();
   return LRAMM_OK;
 }
