@@ -37,6 +37,10 @@ CONFIGS = {
     # BASELINE.json configs[1]
     "c2": dict(m=4096, k=4096, n=4096, rank=256, oversample=16, power_iters=1, bits=(8, 8, 8), tau=128.0,
                mode="fast", sketch_bits=8, power_bits=8, proj_bits=8, granularity="row"),
+    # BASELINE.json configs[3]: 64 independent 2048^3 pairs, r=128, p=10, q=0 (reference default),
+    # int8 sketches with the reference's per-tensor quantiser; batch sharded across ranks
+    "c4": dict(m=2048, k=2048, n=2048, rank=128, oversample=10, power_iters=0, bits=(8, 8, 8), tau=64.0,
+               mode="fast", sketch_bits=8, power_bits=8, proj_bits=8, granularity="tensor", pairs=64, streams=16),
     # BASELINE.json configs[0] (the reference's CPU-runnable case), for quick runs
     "c1": dict(m=1024, k=1024, n=1024, rank=64, oversample=10, power_iters=1, bits=(8, 8, 8), tau=32.0,
                mode="fast", sketch_bits=8, power_bits=8, proj_bits=8, granularity="row"),
@@ -186,14 +190,27 @@ def effective_ops(cfg):
     return 2.0 * cfg["m"] * cfg["n"] * cfg["k"]
 
 
+def pairs_per_rank(cfg, world):
+    total = cfg.get("pairs", 1)
+    if total == 1:
+        return 1
+    if total % world:
+        raise SystemExit(f"{total} pairs do not shard evenly over {world} ranks")
+    return total // world
+
+
 def workload_config(cfg, args, world):
-    return {"workload": f"BASELINE configs[1]: {cfg['m']}x{cfg['k']}x{cfg['n']} fp32 exp:{int(cfg['tau'])} spectrum, "
-                        f"r={cfg['rank']} p={cfg['oversample']} q={cfg['power_iters']}, int8 per-row sketch/power/"
-                        f"projection GEMMs, recombination bits {cfg['bits']}",
+    total = cfg.get("pairs", 1)
+    which = {"c2": "configs[1]", "c4": "configs[3]", "c1": "configs[0]"}[args.config]
+    return {"workload": f"BASELINE {which}: {total} x {cfg['m']}x{cfg['k']}x{cfg['n']} fp32 exp:{int(cfg['tau'])} "
+                        f"spectrum, r={cfg['rank']} p={cfg['oversample']} q={cfg['power_iters']}, int8 "
+                        f"{cfg['granularity']}-scaled sketch/power/projection GEMMs, recombination bits {cfg['bits']}",
             "name": args.config, "m": cfg["m"], "k": cfg["k"], "n": cfg["n"], "rank": cfg["rank"],
             "oversample": cfg["oversample"], "power_iters": cfg["power_iters"], "bits": list(cfg["bits"]),
-            "mode": cfg["mode"], "granularity": cfg["granularity"], "pairs_per_rank": 1,
-            "parallelism": f"{world} independent pair(s), one per rank" if world > 1 else "single GPU",
+            "mode": cfg["mode"], "granularity": cfg["granularity"], "pairs_per_rank": pairs_per_rank(cfg, world),
+            "streams": min(pairs_per_rank(cfg, world), cfg.get("streams", 1)),
+            "parallelism": (f"{world} ranks, independent pairs sharded across ranks (no collective)" if world > 1
+                            else "single GPU"),
             "l2": "inputs (2 x 64 MiB fp32) exceed the 126 MB L2; no explicit flush"}
 
 
@@ -245,29 +262,48 @@ def run_ours(args, cfg, world, rank, local):
         dist.init_process_group("nccl", device_id=dev)
     import paper_2405_16917_b200 as L
 
-    a, b = synth_pair(cfg, rank, dev)
+    P = pairs_per_rank(cfg, world)
+    S = min(P, cfg.get("streams", 1))
+    pairs = [synth_pair(cfg, rank * P + j, dev) for j in range(P)]
+    a, b = pairs[0]
     params = L.LrammParams(rank=cfg["rank"], bits=tuple(cfg["bits"]), power_iters=cfg["power_iters"],
                            oversample=cfg["oversample"], seed=rank, mode=cfg["mode"], sketch_bits=cfg["sketch_bits"],
                            power_bits=cfg["power_bits"], proj_bits=cfg["proj_bits"], granularity=cfg["granularity"],
                            out_dtype=np.float32)
+    outs = [torch.empty((cfg["m"], cfg["n"]), dtype=torch.float32, device=dev) for _ in range(P)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(S)]
+
+    def issue_all():
+        """All pairs of this rank: pair j on stream j % S (each stream has its own workspace)."""
+        cur = torch.cuda.current_stream(dev)
+        evs = []
+        for st_ in streams:
+            st_.wait_stream(cur)
+        for j, (aj, bj) in enumerate(pairs):
+            with torch.cuda.stream(streams[j % S]):
+                _o, status_j, _t = L.lramm_device(aj, bj, params, out=outs[j])
+        for st_ in streams:
+            cur.wait_stream(st_)
+        return status_j
+
     clocks = ClockSampler(local).__enter__()
     time.sleep(0.5)  # nvidia-smi start-up
-    # warm-up (also sets kernel attributes before capture)
+    # warm-up (also sets kernel attributes and allocates per-stream workspaces before capture)
     for _ in range(max(1, args.warmup)):
-        out, status, _t = L.lramm_device(a, b, params)
+        status = issue_all()
     torch.cuda.synchronize()
     st = int(status.item())
     if st:
         raise RuntimeError(f"lramm status {st}")
-    # capture one step into a CUDA graph
-    stream = torch.cuda.Stream(device=dev)
-    stream.wait_stream(torch.cuda.current_stream(dev))
+    # capture one step (all pairs of this rank) into a CUDA graph
+    cap = torch.cuda.Stream(device=dev)
+    cap.wait_stream(torch.cuda.current_stream(dev))
     graph = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(stream):
-        L.lramm_device(a, b, params, out=out)
+    with torch.cuda.stream(cap):
+        issue_all()
         torch.cuda.synchronize()
-        with torch.cuda.graph(graph, stream=stream):
-            L.lramm_device(a, b, params, out=out)
+        with torch.cuda.graph(graph, stream=cap):
+            issue_all()
     torch.cuda.synchronize()
     for _ in range(args.warmup):
         graph.replay()
@@ -296,38 +332,43 @@ def run_ours(args, cfg, world, rank, local):
         ms = float(t.item())
         torch.distributed.barrier()
     ms_per_step = ms / args.steps
-    value = effective_ops(cfg) * world / (ms_per_step * 1e-3) / 1e12
+    value = effective_ops(cfg) * P * world / (ms_per_step * 1e-3) / 1e12
 
     # ---- e2e through the drop-in public API (host buffers, C-ABI host entry point)
-    ha = torch.empty(a.shape, dtype=torch.float32, pin_memory=True)
-    hb = torch.empty(b.shape, dtype=torch.float32, pin_memory=True)
-    ha.copy_(a.cpu())
-    hb.copy_(b.cpu())
-    na, nb = ha.numpy(), hb.numpy()
+    host_pairs = []
+    for aj, bj in pairs:
+        ha = torch.empty(aj.shape, dtype=torch.float32, pin_memory=True)
+        hb = torch.empty(bj.shape, dtype=torch.float32, pin_memory=True)
+        ha.copy_(aj.cpu())
+        hb.copy_(bj.cpu())
+        host_pairs.append((ha.numpy(), hb.numpy()))
     p64 = L.LrammParams(rank=cfg["rank"], bits=tuple(cfg["bits"]), power_iters=cfg["power_iters"],
                         oversample=cfg["oversample"], seed=rank, mode=cfg["mode"], sketch_bits=cfg["sketch_bits"],
                         power_bits=cfg["power_bits"], proj_bits=cfg["proj_bits"], granularity=cfg["granularity"])
     hout = torch.empty((cfg["m"], cfg["n"]), dtype=torch.float64, pin_memory=True).numpy()
     for _ in range(max(1, min(args.warmup, 2))):
-        L.lramm(na, nb, p64, out=hout)
-    e2e_steps = max(1, min(args.steps, 5))
+        L.lramm(host_pairs[0][0], host_pairs[0][1], p64, out=hout)
+    e2e_steps = max(1, min(args.steps, 5 if P == 1 else 1))
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        d, _ = L.lramm(na, nb, p64, out=hout)
+        for na, nb in host_pairs:
+            d, _ = L.lramm(na, nb, p64, out=hout)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     if world > 1:
         t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
     wa = min(cfg["rank"] + cfg["oversample"], cfg["k"])
-    h2d = 4 * (cfg["m"] * cfg["k"] + cfg["k"] * cfg["n"]) + 8 * (cfg["k"] * wa + cfg["n"] * wa)
-    d2h = 8 * cfg["m"] * cfg["n"]
-    e2e = {"value": effective_ops(cfg) * world / e2e_s / 1e12, "unit": "TOPS", "h2d_bytes_per_step": h2d,
+    h2d = P * (4 * (cfg["m"] * cfg["k"] + cfg["k"] * cfg["n"]) + 8 * (cfg["k"] * wa + cfg["n"] * wa))
+    d2h = P * 8 * cfg["m"] * cfg["n"]
+    e2e = {"value": effective_ops(cfg) * P * world / e2e_s / 1e12, "unit": "TOPS", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
-           "path": "lramm(numpy) -> lramm_host_lramm (C ABI), pinned A/B/D, fp64 D like the reference"}
+           "path": "lramm(numpy) -> lramm_host_lramm (C ABI), pinned A/B/D, fp64 D like the reference"
+                   + ("; pairs issued one after another" if P > 1 else "")}
 
     # ---- dominant kernel + launches (live, torch profiler over device-resident steps)
     top_name, top_us, top_per_step, step_us, launches, per = roofline_probe(L, a, b, params)
+    launches *= P  # per step = all pairs of this rank
     peaks = measured_peaks()
     roof = dominant_roofline(top_name, top_us, cfg, peaks)
     roof["kernel"] = top_name

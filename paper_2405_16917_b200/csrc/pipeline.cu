@@ -12,6 +12,8 @@
 // and the lift are fp64, and the recombination E1 -> E2 -> E3 uses the
 // reference's per-tensor quantiser at (d1, d2, d3) with int8 tcgen05 GEMMs.
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -327,22 +329,23 @@ __global__ void gather_info_kernel(const int *a, const int *b, const int *ca, co
   if (nfa[0] || nfb[0]) nonfinite[0] = 1;
 }
 
-// per-thread, per-device side stream + fork/join events
+// side stream + fork/join events per caller stream (so independent lramm() calls issued on
+// different streams -- e.g. the pairs of a batch -- do not serialise on a shared side stream)
 struct SideStream {
   cudaStream_t st = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
-  int dev = -1;
 };
-SideStream &side_stream() {
-  static thread_local SideStream s[16];
+SideStream &side_stream(cudaStream_t main) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, SideStream> table;
   int dev = 0;
   cudaGetDevice(&dev);
-  SideStream &x = s[dev & 15];
-  if (x.dev != dev) {
+  std::lock_guard<std::mutex> g(mu);
+  SideStream &x = table[{dev, main}];
+  if (!x.st) {
     cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
-    x.dev = dev;
   }
   return x;
 }
@@ -420,7 +423,7 @@ int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t 
   LRAMM_TRY(mark(0));
   // ---- rsvd of both operands (pipeline.py:183-186): independent chains, so B runs on a
   // forked side stream (event fork/join; capturable into a CUDA graph)
-  SideStream &side = side_stream();
+  SideStream &side = side_stream(st);
   LRAMM_CUDA_TRY(cudaEventRecord(side.fork, st));
   LRAMM_CUDA_TRY(cudaStreamWaitEvent(side.st, side.fork, 0));
   LRAMM_TRY(run_rsvd(b, in_dtype, L.rb, P, omega_b, L.UB, r, L.SB, L.VB, r, side.st));
