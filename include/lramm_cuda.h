@@ -127,6 +127,27 @@ int lramm_quantize(const void *x, int x_dtype, int64_t rows, int64_t cols, int64
                    lramm_stream_t stream);
 size_t lramm_quantize_ws(int64_t rows, int64_t cols);
 
+/* max |x| per tensor / row / column (exact; amax must be zeroed by the caller: the kernel takes a
+ * max into it, so partial results of several shards can be combined with an allreduce(MAX)). */
+int lramm_absmax(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int granularity, double *amax,
+                 int *nonfinite_flag, lramm_stream_t stream);
+
+/* lramm_quantize with externally supplied amax (e.g. allreduced across shards): scale = cap/amax. */
+int lramm_quantize_amax(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits,
+                        int granularity, int transpose_out, const double *amax, void *q, int q_dtype, int64_t ldq,
+                        double *scales, lramm_stream_t stream);
+
+/* One CholeskyQR pass with a Gram matrix G = Y^T Y supplied by the caller (e.g. summed over row
+ * shards): L = chol(G) (lower, w x w), q = y L^-T.  info (device int): 0 ok, j+1 on breakdown. */
+int lramm_cholqr_pass(const double *y, int64_t m, int64_t w, int64_t ldy, const double *gram, double *q, int64_t ldq,
+                      double *l, int *info, void *ws, size_t ws_bytes, lramm_stream_t stream);
+size_t lramm_cholqr_pass_ws(int64_t m, int64_t w);
+
+/* Dequantising epilogue over an int32 accumulator matrix (e.g. partial products summed across
+ * shards): same semantics as lramm_igemm's epilogue. */
+int lramm_dequant(const int32_t *acc, int64_t M, int64_t N, int64_t lda, const lramm_epilogue_t *epi,
+                  lramm_stream_t stream);
+
 /* rint(a*scale) half-to-even, clamp +-cap, int32 (the plugin kernel, _core.pyx:53-69). */
 int lramm_scale_round_clip(const double *a, int64_t rows, int64_t cols, int64_t lda, double scale,
                            int cap, int32_t *out, int64_t ldo, lramm_stream_t stream);

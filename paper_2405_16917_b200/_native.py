@@ -83,6 +83,11 @@ SIGNATURES = {
     "lramm_quantize": (_i32, [_vp, _i32, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _i32, _i64, _vp, _vp, _vp, _sz, _vp]),
     "lramm_quantize_ws": (_sz, [_i64, _i64]),
     "lramm_scale_round_clip": (_i32, [_vp, _i64, _i64, _i64, _d, _i32, _vp, _i64, _vp]),
+    "lramm_absmax": (_i32, [_vp, _i32, _i64, _i64, _i64, _i32, _vp, _vp, _vp]),
+    "lramm_quantize_amax": (_i32, [_vp, _i32, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _i32, _i64, _vp, _vp]),
+    "lramm_cholqr_pass": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "lramm_cholqr_pass_ws": (_sz, [_i64, _i64]),
+    "lramm_dequant": (_i32, [_vp, _i64, _i64, _i64, _P(Epilogue), _vp]),
     "lramm_igemm": (_i32, [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _P(Epilogue), _i32, _vp]),
     "lramm_dgemm": (_i32, [_i32, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _sz, _vp]),
     "lramm_dgemm_ws": (_sz, [_i32, _i64, _i64, _i64]),
@@ -107,7 +112,7 @@ SIGNATURES = {
 def _load():
     if not os.path.exists(LIB_PATH):
         raise NativeLibraryMissing(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2405_16917_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_2405_16917_b200/build.py` "
             "(there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():

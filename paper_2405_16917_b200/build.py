@@ -1,6 +1,6 @@
 """Build liblramm_cuda.so in-tree with nvcc for sm_100a (no JIT, no torch extension).
 
-    python -m paper_2405_16917_b200.build        # or __graft_entry__.build()
+    python paper_2405_16917_b200/build.py        # or __graft_entry__.build()
 """
 
 from __future__ import annotations

@@ -45,6 +45,13 @@ int num_sms() {
 int quantize_device(const void *, int, int64_t, int64_t, int64_t, int, int, int, void *, int, int64_t, double *, int *,
                     void *, size_t, cudaStream_t);
 size_t quantize_ws_bytes(int64_t, int64_t);
+int absmax_device(const void *, int, int64_t, int64_t, int64_t, int, double *, int *, cudaStream_t);
+int quantize_amax_device(const void *, int, int64_t, int64_t, int64_t, int, int, int, const double *, void *, int, int64_t,
+                         double *, cudaStream_t);
+int cholqr_pass_device(const double *, int64_t, int64_t, int64_t, const double *, double *, int64_t, double *, int *,
+                       void *, size_t, cudaStream_t);
+size_t cholqr_pass_ws_bytes(int64_t, int64_t);
+int epilogue_device(const int32_t *, int64_t, int64_t, int64_t, const lramm_epilogue_t &, cudaStream_t);
 int scale_round_clip_device(const double *, int64_t, int64_t, int64_t, double, int, int32_t *, int64_t, cudaStream_t);
 int igemm_device(int64_t, int64_t, int64_t, const int8_t *, int64_t, const int8_t *, int64_t, const lramm_epilogue_t &,
                  int, cudaStream_t);
@@ -128,6 +135,30 @@ int lramm_quantize(const void *x, int x_dtype, int64_t rows, int64_t cols, int64
                          nonfinite_flag, ws, ws_bytes, (cudaStream_t)stream);
 }
 size_t lramm_quantize_ws(int64_t rows, int64_t cols) { return quantize_ws_bytes(rows, cols); }
+
+int lramm_absmax(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int granularity, double *amax,
+                 int *nonfinite_flag, lramm_stream_t stream) {
+  return absmax_device(x, x_dtype, rows, cols, ldx, granularity, amax, nonfinite_flag, (cudaStream_t)stream);
+}
+
+int lramm_quantize_amax(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits,
+                        int granularity, int transpose_out, const double *amax, void *q, int q_dtype, int64_t ldq,
+                        double *scales, lramm_stream_t stream) {
+  return quantize_amax_device(x, x_dtype, rows, cols, ldx, bits, granularity, transpose_out, amax, q, q_dtype, ldq,
+                              scales, (cudaStream_t)stream);
+}
+
+int lramm_cholqr_pass(const double *y, int64_t m, int64_t w, int64_t ldy, const double *gram, double *q, int64_t ldq,
+                      double *l, int *info, void *ws, size_t ws_bytes, lramm_stream_t stream) {
+  return cholqr_pass_device(y, m, w, ldy, gram, q, ldq, l, info, ws, ws_bytes, (cudaStream_t)stream);
+}
+size_t lramm_cholqr_pass_ws(int64_t m, int64_t w) { return cholqr_pass_ws_bytes(m, w); }
+
+int lramm_dequant(const int32_t *acc, int64_t M, int64_t N, int64_t lda, const lramm_epilogue_t *epi,
+                  lramm_stream_t stream) {
+  if (!epi) return fail(LRAMM_ERR_PARAM, "dequant: epilogue is NULL");
+  return epilogue_device(acc, M, N, lda, *epi, (cudaStream_t)stream);
+}
 
 int lramm_scale_round_clip(const double *a, int64_t rows, int64_t cols, int64_t lda, double scale, int cap, int32_t *out,
                            int64_t ldo, lramm_stream_t stream) {

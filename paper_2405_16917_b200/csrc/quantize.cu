@@ -169,15 +169,8 @@ __global__ void scale_round_clip_kernel(const double *__restrict__ a, int64_t ro
 }
 
 template <class T>
-int quantize_impl(const T *x, int64_t rows, int64_t cols, int64_t ldx, int bits, int gran, int transpose,
-                  void *q, int q_dtype, int64_t ldq, double *scales, int *nonfinite, void *ws,
-                  size_t ws_bytes, cudaStream_t st) {
-  const int cap = bit_cap(bits);
-  const int64_t nscale = gran == LRAMM_GRAN_TENSOR ? 1 : (gran == LRAMM_GRAN_ROW ? rows : cols);
-  Arena ar(ws, ws_bytes);
-  double *amax = ar.take<double>(nscale);
-  if (!ar.ok() || amax == nullptr) return fail(LRAMM_ERR_WORKSPACE, "quantize: workspace too small");
-  LRAMM_CUDA_TRY(cudaMemsetAsync(amax, 0, nscale * sizeof(double), st));
+int absmax_launch(const T *x, int64_t rows, int64_t cols, int64_t ldx, int gran, double *amax, int *nonfinite,
+                  cudaStream_t st) {
   const int sms = num_sms();
   if (gran == LRAMM_GRAN_TENSOR) {
     int grid = (int)std::min<int64_t>(rows, 8LL * sms);
@@ -190,6 +183,14 @@ int quantize_impl(const T *x, int64_t rows, int64_t cols, int64_t ldx, int bits,
     absmax_cols_kernel<T><<<grid, dim3(32, 8), 0, st>>>(x, rows, cols, ldx, chunk, amax, nonfinite);
   }
   LRAMM_LAUNCH_CHECK();
+  return LRAMM_OK;
+}
+
+template <class T>
+int quantize_from_amax(const T *x, int64_t rows, int64_t cols, int64_t ldx, int bits, int gran, int transpose,
+                       const double *amax, void *q, int q_dtype, int64_t ldq, double *scales, cudaStream_t st) {
+  const int cap = bit_cap(bits);
+  const int64_t nscale = gran == LRAMM_GRAN_TENSOR ? 1 : (gran == LRAMM_GRAN_ROW ? rows : cols);
   scales_from_amax_kernel<<<(unsigned)ceil_div(nscale, 256), 256, 0, st>>>(amax, nscale, cap, scales);
   LRAMM_LAUNCH_CHECK();
   const int64_t out_rows = transpose ? cols : rows;
@@ -212,6 +213,19 @@ int quantize_impl(const T *x, int64_t rows, int64_t cols, int64_t ldx, int bits,
   return LRAMM_OK;
 }
 
+template <class T>
+int quantize_impl(const T *x, int64_t rows, int64_t cols, int64_t ldx, int bits, int gran, int transpose,
+                  void *q, int q_dtype, int64_t ldq, double *scales, int *nonfinite, void *ws,
+                  size_t ws_bytes, cudaStream_t st) {
+  const int64_t nscale = gran == LRAMM_GRAN_TENSOR ? 1 : (gran == LRAMM_GRAN_ROW ? rows : cols);
+  Arena ar(ws, ws_bytes);
+  double *amax = ar.take<double>(nscale);
+  if (!ar.ok() || amax == nullptr) return fail(LRAMM_ERR_WORKSPACE, "quantize: workspace too small");
+  LRAMM_CUDA_TRY(cudaMemsetAsync(amax, 0, nscale * sizeof(double), st));
+  LRAMM_TRY(absmax_launch<T>(x, rows, cols, ldx, gran, amax, nonfinite, st));
+  return quantize_from_amax<T>(x, rows, cols, ldx, bits, gran, transpose, amax, q, q_dtype, ldq, scales, st);
+}
+
 }  // namespace
 
 int quantize_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits,
@@ -232,6 +246,30 @@ int quantize_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int6
   if (x_dtype == LRAMM_F64)
     return quantize_impl<double>((const double *)x, rows, cols, ldx, bits, gran, transpose, q, q_dtype, ldq,
                                  scales, nonfinite, ws, ws_bytes, st);
+  return fail(LRAMM_ERR_PARAM, "quantize: input dtype must be F32 or F64");
+}
+
+int absmax_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int gran, double *amax,
+                  int *nonfinite, cudaStream_t st) {
+  if (rows < 1 || cols < 1 || ldx < cols) return fail(LRAMM_ERR_SHAPE, "absmax: bad shape");
+  if (gran < 0 || gran > 2) return fail(LRAMM_ERR_PARAM, "bad granularity %d", gran);
+  if (x_dtype == LRAMM_F32) return absmax_launch<float>((const float *)x, rows, cols, ldx, gran, amax, nonfinite, st);
+  if (x_dtype == LRAMM_F64) return absmax_launch<double>((const double *)x, rows, cols, ldx, gran, amax, nonfinite, st);
+  return fail(LRAMM_ERR_PARAM, "absmax: input dtype must be F32 or F64");
+}
+
+int quantize_amax_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits, int gran,
+                         int transpose, const double *amax, void *q, int q_dtype, int64_t ldq, double *scales,
+                         cudaStream_t st) {
+  if (rows < 1 || cols < 1 || ldx < cols) return fail(LRAMM_ERR_SHAPE, "quantize: bad shape");
+  if (bits < 2 || bits > 24) return fail(LRAMM_ERR_PARAM, "bits must be an integer in [2, 24], got %d", bits);
+  if (q_dtype == LRAMM_I8 && bits > 8) return fail(LRAMM_ERR_UNSUPPORTED, "int8 output needs bits <= 8");
+  if (x_dtype == LRAMM_F32)
+    return quantize_from_amax<float>((const float *)x, rows, cols, ldx, bits, gran, transpose, amax, q, q_dtype, ldq,
+                                     scales, st);
+  if (x_dtype == LRAMM_F64)
+    return quantize_from_amax<double>((const double *)x, rows, cols, ldx, bits, gran, transpose, amax, q, q_dtype,
+                                      ldq, scales, st);
   return fail(LRAMM_ERR_PARAM, "quantize: input dtype must be F32 or F64");
 }
 

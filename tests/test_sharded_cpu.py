@@ -1,0 +1,187 @@
+"""Sharded LRAMM (A row-sharded, B column-sharded) over gloo, world_size 1 and 2, on CPU.
+
+The orchestration in `paper_2405_16917_b200/sharded.py` is run with NumPy shard ops
+built from the oracle's quantiser (test infrastructure), so the collective logic —
+which scales are allreduced, which partial products are summed, the E2 allgather —
+is checked against the single-process oracle `lramm()` without a GPU.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import lramm_oracle as O
+
+from paper_2405_16917_b200.pipeline import LrammParams
+from paper_2405_16917_b200.sharded import Comm, lramm_sharded, shard_bounds
+
+
+class NumpyOps:
+    """The CudaOps interface on CPU tensors, arithmetic from the oracle (quant.py semantics)."""
+
+    def f64(self, shape):
+        return torch.empty(shape, dtype=torch.float64)
+
+    def omega(self, seed, n, w):
+        return torch.from_numpy(O.gaussian_sketch(seed, n, w))
+
+    def absmax(self, x, gran):
+        a = np.abs(x.double().numpy())
+        if gran == "tensor":
+            v = np.array([a.max() if a.size else 0.0])
+        else:
+            v = a.max(axis=1 if gran == "row" else 0)
+        return torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64))
+
+    def quantize(self, x, bits, gran, transpose, amax):
+        a = x.double().numpy()
+        cap = O.bit_cap(bits)
+        am = amax.numpy()
+        scale = np.ones_like(am)
+        nz = am != 0.0
+        scale[nz] = float(cap) / am[nz]
+        s = scale[0] if gran == "tensor" else (scale[:, None] if gran == "row" else scale[None, :])
+        q = O.scale_round_clip(a, s, cap).astype(np.int8)
+        if transpose:
+            q = q.T
+        return torch.from_numpy(np.ascontiguousarray(q)), torch.from_numpy(scale)
+
+    def iprod(self, qa, qb, M, N, K):
+        acc = qa.numpy()[:, :K].astype(np.int64) @ qb.numpy()[:, :K].astype(np.int64).T
+        return torch.from_numpy(acc.astype(np.int32))
+
+    def dequant(self, acc, sa, sb, out_dtype=torch.float64, transpose=False, alpha=1.0, beta=0.0, c=None):
+        sa, sb = sa.numpy(), sb.numpy()
+        out = acc.numpy().astype(np.float64) / (sa[:, None] * sb[None, :])
+        if beta != 0.0 and c is not None:
+            out = alpha * out + beta * c.double().numpy()
+        elif alpha != 1.0:
+            out = alpha * out
+        if transpose:
+            out = out.T
+        return torch.from_numpy(np.ascontiguousarray(out))
+
+    def gemm(self, trans_a, a, b):
+        a, b = a.double().numpy(), b.double().numpy()
+        return torch.from_numpy(np.ascontiguousarray((a.T if trans_a else a) @ b))
+
+    def cholqr_pass(self, y, gram):
+        lo = np.linalg.cholesky(gram.numpy())
+        q = np.linalg.solve(lo, y.numpy().T).T
+        return torch.from_numpy(np.ascontiguousarray(q)), torch.from_numpy(lo), torch.zeros(1, dtype=torch.int32)
+
+    def qr(self, y):
+        return torch.from_numpy(np.ascontiguousarray(np.linalg.qr(y.numpy())[0]))
+
+    def svd(self, a):
+        u, s, v = O.svd(a.numpy())
+        return torch.from_numpy(u), torch.from_numpy(np.ascontiguousarray(s)), torch.from_numpy(v)
+
+
+def _inputs(m, k, n, seed):
+    a = O.synth(m, k, "exp:6", 90, seed, 0)
+    b = O.synth(k, n, "exp:6", 90, seed, 1)
+    return a.astype(np.float64), b.astype(np.float64)
+
+
+def _worker(rank, world, port, case, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        (m, k, n), kw = case
+        a, b = _inputs(m, k, n, 7)
+        c = np.linspace(-1, 1, m * n).reshape(m, n) if kw.get("beta") else None
+        (ma, mb), (na, nb) = shard_bounds(m, n, world, rank)
+        params = LrammParams(**kw)
+        comm = Comm()
+        d = lramm_sharded(torch.from_numpy(a[ma:mb].copy()), torch.from_numpy(b[:, na:nb].copy()), (m, k, n),
+                          params, comm=comm, ops=NumpyOps(),
+                          c_rows=None if c is None else torch.from_numpy(c[ma:mb].copy()))
+        full = comm.gather_rows(d)
+        if rank == 0:
+            out_q.put(full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _run(world, case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    import queue
+    import time
+
+    deadline = time.time() + 240
+    while True:
+        try:
+            out = q.get(timeout=1)
+            break
+        except queue.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs) or time.time() > deadline:
+                for p in procs:
+                    p.kill()
+                raise AssertionError(f"sharded worker failed: exit codes {[p.exitcode for p in procs]}")
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    return out
+
+
+CASES = [
+    ((96, 80, 72), dict(rank=8, mode="parity")),
+    ((96, 80, 72), dict(rank=8, mode="fast", granularity="row", power_iters=1)),
+    ((90, 64, 77), dict(rank=6, mode="fast", granularity="tensor", alpha=0.5, beta=2.0)),
+]
+
+
+def _oracle(case):
+    (m, k, n), kw = case
+    a, b = _inputs(m, k, n, 7)
+    c = np.linspace(-1, 1, m * n).reshape(m, n) if kw.get("beta") else None
+    fast = kw.get("mode") == "fast"
+    spec = O.SketchSpec(8, 8, 8, kw.get("granularity", "tensor")) if fast else O.SketchSpec()
+    p = O.OracleParams(rank=kw["rank"], power_iters=kw.get("power_iters", 0), alpha=kw.get("alpha", 1.0),
+                       beta=kw.get("beta", 0.0), spec=spec)
+    return O.lramm(a, b, p, c=c), a @ b * kw.get("alpha", 1.0) + (kw.get("beta", 0.0) * c if c is not None else 0)
+
+
+@pytest.mark.parametrize("case", CASES, ids=["parity", "fast-row-q1", "fast-tensor-ab"])
+def test_sharded_world2_matches_oracle(case):
+    d2 = _run(2, case)
+    ref, exact = _oracle(case)
+    assert d2.shape == ref.shape
+    err = O.rel_fro(d2, ref)
+    assert err <= 1e-3, err
+    # and it is the same approximation: its error to the exact product matches the oracle's
+    assert abs(O.rel_fro(d2, exact) - O.rel_fro(ref, exact)) <= 1e-3
+
+
+def test_sharded_world1_equals_world2_fast():
+    """Fast mode: int32 partials are summed exactly, so world sizes agree to fp64 rounding of the Grams."""
+    case = CASES[1]
+    d1 = _run(1, case)
+    d2 = _run(2, case)
+    assert O.rel_fro(d2, d1) <= 1e-9
+
+
+def test_shard_bounds_cover():
+    for m, n, w in [(10, 7, 3), (5, 5, 5), (128, 64, 8)]:
+        rows = [shard_bounds(m, n, w, r)[0] for r in range(w)]
+        cols = [shard_bounds(m, n, w, r)[1] for r in range(w)]
+        assert rows[0][0] == 0 and rows[-1][1] == m and cols[-1][1] == n
+        assert all(rows[i][1] == rows[i + 1][0] for i in range(w - 1))
