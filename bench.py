@@ -44,6 +44,13 @@ CONFIGS = {
     # BASELINE.json configs[0] (the reference's CPU-runnable case), for quick runs
     "c1": dict(m=1024, k=1024, n=1024, rank=64, oversample=10, power_iters=1, bits=(8, 8, 8), tau=32.0,
                mode="fast", sketch_bits=8, power_bits=8, proj_bits=8, granularity="row"),
+    # BASELINE.json configs[2]: polynomial spectrum, int4 per-row sketch Y = A.Omega, int8 elsewhere
+    "c3": dict(m=8192, k=8192, n=8192, rank=512, oversample=32, power_iters=2, bits=(8, 8, 8), poly=1.5,
+               mode="fast", sketch_bits=4, power_bits=8, proj_bits=8, granularity="row"),
+    # BASELINE.json configs[4]: tall-skinny; at N > 1 A is row-sharded and B column-sharded
+    # (paper_2405_16917_b200/sharded.py), at N = 1 the whole problem runs on one GPU
+    "c5": dict(m=131072, k=8192, n=8192, rank=1024, oversample=32, power_iters=1, bits=(8, 8, 8), tau=256.0,
+               mode="fast", sketch_bits=8, power_bits=8, proj_bits=8, granularity="tensor", sharded=True),
 }
 
 
@@ -54,26 +61,32 @@ def dist_env():
     return world, rank, local
 
 
+def spectrum_name(cfg):
+    return f"poly:{cfg['poly']}" if "poly" in cfg else f"exp:{int(cfg['tau'])}"
+
+
 def synth_pair(cfg, seed, device):
-    """A = U diag(sigma) V^T, B likewise; Haar U, V (QR of seeded Gaussians, sign-fixed);
-    sigma_i = exp(-i/tau) + 1e-4; stored fp32."""
+    """A = U diag(sigma) V^T, B likewise; Haar U, V (thin QR of seeded Gaussians, sign-fixed);
+    sigma_i = exp(-i/tau) + 1e-4 or i^-alpha; stored fp32."""
     import torch
 
     g = torch.Generator(device=device)
     g.manual_seed(0x1A3A * 1000 + seed)
 
-    def haar(n):
-        z = torch.randn(n, n, generator=g, device=device, dtype=torch.float64)
+    def haar(n, t):
+        z = torch.randn(n, t, generator=g, device=device, dtype=torch.float64)
         q, r = torch.linalg.qr(z)
         return q * torch.sign(torch.diagonal(r))
 
     def mat(rows, cols):
         t = min(rows, cols)
         i = torch.arange(1, t + 1, device=device, dtype=torch.float64)
-        sig = torch.exp(-i / cfg["tau"]) + 1e-4
-        u = haar(rows)[:, :t]
-        v = haar(cols)[:, :t]
-        return ((u * sig) @ v.T).to(torch.float32).contiguous()
+        sig = i ** (-cfg["poly"]) if "poly" in cfg else torch.exp(-i / cfg["tau"]) + 1e-4
+        u = haar(rows, t)
+        v = haar(cols, t)
+        out = ((u * sig) @ v.T).to(torch.float32).contiguous()
+        del u, v
+        return out
 
     return mat(cfg["m"], cfg["k"]), mat(cfg["k"], cfg["n"])
 
@@ -142,16 +155,17 @@ def measured_peaks():
 
 # ------------------------------------------------------------------ roofline of the dominant kernel
 
-def roofline_probe(L, ta, tb, params, reps=5):
+def roofline_probe(L, ta, tb, params, reps=5, step=None):
     """Time the hot path's kernels live (torch profiler over one step), pick the dominant one and
     express it against its roofline."""
     import torch
     from torch.profiler import ProfilerActivity, profile
 
+    step = step or (lambda: L.lramm_device(ta, tb, params))
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(reps):
-            L.lramm_device(ta, tb, params)
+            step()
         torch.cuda.synchronize()
     per = {}
     launches = 0
@@ -178,11 +192,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the row/column-sharded path (default for c5 at N > 1) even at N = 1")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, cfg, world, rank)
+    if args.sharded or (cfg.get("sharded") and world > 1):
+        return run_sharded(args, cfg, world, rank, local)
     return run_ours(args, cfg, world, rank, local)
 
 
@@ -201,21 +219,34 @@ def pairs_per_rank(cfg, world):
 
 def workload_config(cfg, args, world):
     total = cfg.get("pairs", 1)
-    which = {"c2": "configs[1]", "c4": "configs[3]", "c1": "configs[0]"}[args.config]
-    return {"workload": f"BASELINE {which}: {total} x {cfg['m']}x{cfg['k']}x{cfg['n']} fp32 exp:{int(cfg['tau'])} "
-                        f"spectrum, r={cfg['rank']} p={cfg['oversample']} q={cfg['power_iters']}, int8 "
+    which = {"c1": "configs[0]", "c2": "configs[1]", "c3": "configs[2]", "c4": "configs[3]",
+             "c5": "configs[4]"}[args.config]
+    sharded = cfg.get("sharded") and world > 1
+    return {"workload": f"BASELINE {which}: {total} x {cfg['m']}x{cfg['k']}x{cfg['n']} fp32 {spectrum_name(cfg)} "
+                        f"spectrum, r={cfg['rank']} p={cfg['oversample']} q={cfg['power_iters']}, "
+                        f"int{cfg['sketch_bits']}/int{cfg['power_bits']}/int{cfg['proj_bits']} "
                         f"{cfg['granularity']}-scaled sketch/power/projection GEMMs, recombination bits {cfg['bits']}",
             "name": args.config, "m": cfg["m"], "k": cfg["k"], "n": cfg["n"], "rank": cfg["rank"],
             "oversample": cfg["oversample"], "power_iters": cfg["power_iters"], "bits": list(cfg["bits"]),
             "mode": cfg["mode"], "granularity": cfg["granularity"], "pairs_per_rank": pairs_per_rank(cfg, world),
             "streams": min(pairs_per_rank(cfg, world), cfg.get("streams", 1)),
-            "parallelism": (f"{world} ranks, independent pairs sharded across ranks (no collective)" if world > 1
+            "parallelism": (f"{world} ranks, A row-sharded / B column-sharded, NCCL Gram + int32 partial "
+                            f"allreduces, E2 allgather" if sharded else
+                            f"{world} ranks, independent pairs sharded across ranks (no collective)" if world > 1
                             else "single GPU"),
-            "l2": "inputs (2 x 64 MiB fp32) exceed the 126 MB L2; no explicit flush"}
+            "l2": f"inputs ({(cfg['m'] * cfg['k'] + cfg['k'] * cfg['n']) * 4 / 2**20:.0f} MiB fp32) exceed the "
+                  f"126 MB L2; no explicit flush"}
+
+
+CPU_SAMPLE_CONFIGS = ("c1", "c2", "c4")  # the reference finishes these within minutes
 
 
 def run_reference(args, cfg, world, rank):
     if rank != 0:
+        return 0
+    if args.config not in CPU_SAMPLE_CONFIGS:
+        print(json.dumps({"impl": "reference", "unavailable": f"the reference CPU path needs hours at "
+                          f"{args.config} (SURVEY K10: c3 433 s, c5 ~3.6 h per call); run --config c2"}))
         return 0
     sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
     try:
@@ -383,8 +414,106 @@ def run_ours(args, cfg, world, rank, local):
             "data": "synthetic (SURVEY §8(d) spectrum, Haar factors from seeded torch QR)",
             "config": workload_config(cfg, args, world), "clocks": clock_summary, "e2e": e2e,
             "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches, "roofline": roof}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in CPU_SAMPLE_CONFIGS:
         line["cpu_baseline"] = cpu_baseline(cfg, a, b)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def run_sharded(args, cfg, world, rank, local):
+    """One approximate GEMM per step with A row-sharded and B column-sharded over the ranks
+    (SURVEY §8(e)); value = 2mnk / (max-over-ranks device time), strong scaling."""
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2405_16917_b200 as L
+    from paper_2405_16917_b200.sharded import Comm, CudaOps, lramm_sharded, shard_bounds
+
+    m, k, n = cfg["m"], cfg["k"], cfg["n"]
+    a, b = synth_pair(cfg, 0, dev)  # same seed on every rank: each keeps its own slice
+    (ma, mb), (na, nb) = shard_bounds(m, n, world, rank)
+    a_i, b_j = a[ma:mb].contiguous(), b[:, na:nb].contiguous()
+    del a, b
+    torch.cuda.empty_cache()
+    params = L.LrammParams(rank=cfg["rank"], bits=tuple(cfg["bits"]), power_iters=cfg["power_iters"],
+                           oversample=cfg["oversample"], seed=0, mode=cfg["mode"], sketch_bits=cfg["sketch_bits"],
+                           power_bits=cfg["power_bits"], proj_bits=cfg["proj_bits"], granularity=cfg["granularity"])
+    comm, ops = Comm(), CudaOps(local)
+
+    def step():
+        return lramm_sharded(a_i, b_j, (m, k, n), params, comm=comm, ops=ops)
+
+    clocks = ClockSampler(local).__enter__()
+    time.sleep(0.5)
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk_mark = clocks.mark()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clocks.__exit__(None, None, None)
+    clock_summary = clocks.summary(clk_mark)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = effective_ops(cfg) / (ms_per_step * 1e-3) / 1e12
+
+    # e2e: this rank's shards from pinned host memory, D rows back to the host, every step
+    ha = torch.empty(a_i.shape, dtype=torch.float32, pin_memory=True)
+    hb = torch.empty(b_j.shape, dtype=torch.float32, pin_memory=True)
+    ha.copy_(a_i)
+    hb.copy_(b_j)
+    hd = torch.empty((mb - ma, n), dtype=torch.float64, pin_memory=True)
+    e2e_steps = max(1, min(args.steps, 3))
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        da, db = ha.to(dev, non_blocking=True), hb.to(dev, non_blocking=True)
+        d = lramm_sharded(da, db, (m, k, n), params, comm=comm, ops=ops)
+        hd.copy_(d)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": effective_ops(cfg) / e2e_s / 1e12, "unit": "TOPS",
+           "h2d_bytes_per_step": 4 * (a_i.numel() + b_j.numel()), "d2h_bytes_per_step": 8 * hd.numel(),
+           "ms_per_step": e2e_s * 1e3, "path": "sharded lramm on this rank's pinned host shards, fp64 D rows"}
+    top_name, top_us, top_per_step, step_us, launches, _ = roofline_probe(L, None, None, None, reps=2, step=step)
+    roof = dominant_roofline(top_name, top_us, cfg, measured_peaks())
+    roof.update(kernel=top_name, us_per_launch=top_us, launches_per_step=top_per_step,
+                share_of_step=top_us * top_per_step / step_us if step_us else None)
+    line = {"metric": "effective approx-GEMM TOPS (2mnk/time)", "value": value, "unit": "TOPS", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "int8 x int8 -> int32 (tcgen05) sketch/QM GEMMs; fp64 factorisation; fp64 D",
+            "data": "synthetic (SURVEY §8(d) spectrum, Haar factors from seeded torch QR)",
+            "config": dict(workload_config(cfg, args, world), parallelism=(
+                f"{world} ranks, A row-sharded / B column-sharded, Gram + int32 partial allreduces, E2 allgather"
+                if world > 1 else "sharded code path at world size 1 (no collectives)")),
+            "clocks": clock_summary, "e2e": e2e, "gpu_launches": launches * args.steps,
+            "gpu_launches_per_step": launches, "roofline": roof}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

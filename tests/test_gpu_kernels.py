@@ -220,7 +220,7 @@ def test_dgemm_transposed_split_k(N):
     assert np.array_equal(got, got2)  # deterministic split-K
 
 
-@pytest.mark.parametrize("mw", [(200, 16), (4096, 272), (1000, 74), (333, 100)])
+@pytest.mark.parametrize("mw", [(200, 16), (4096, 272), (1000, 74), (333, 100), (2048, 544), (3000, 1056)])
 def test_qr_orthonormal_and_spans(mw):
     from paper_2405_16917_b200.rsvd import _qr_device
 
@@ -245,7 +245,8 @@ def test_qr_rank_deficient_falls_back_to_householder():
     assert np.linalg.norm(y - q @ (q.T @ y)) <= 1e-12
 
 
-@pytest.mark.parametrize("shape", [(20, 20), (35, 14), (14, 35), (300, 74), (4096, 272), (1000, 138), (90, 520)])
+@pytest.mark.parametrize("shape", [(20, 20), (35, 14), (14, 35), (300, 74), (4096, 272), (1000, 138), (90, 520),
+                                   (1200, 544), (1100, 1056)])
 def test_svd_contracts(shape):
     from paper_2405_16917_b200 import kernels
 
