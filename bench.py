@@ -180,6 +180,8 @@ def roofline_probe(L, ta, tb, params, reps=5, step=None):
         d[0] += ev.device_time
         d[1] += 1
     total = sum(v[0] for v in per.values())
+    if not per:  # no CUPTI events (e.g. running under ncu, which owns the profiler)
+        return "unavailable (profiler busy)", 0.0, 0, 0.0, 0, per
     top = max(per.items(), key=lambda kv: kv[1][0])
     return top[0], top[1][0] / top[1][1], top[1][1] // reps, total / reps, launches // reps, per
 
@@ -523,6 +525,8 @@ def run_sharded(args, cfg, world, rank, local):
 
 def dominant_roofline(name, us, cfg, peaks):
     """Algorithmic work of the dominant kernel per launch over its measured time."""
+    if not us:
+        return {"bound": None, "achieved": None, "peak": None, "unit": None, "frac": None, "traffic": None}
     m, k, n, r = cfg["m"], cfg["k"], cfg["n"], cfg["rank"]
     w = r + cfg["oversample"]
     fp64_peak = 36.7  # TFLOP/s, DFMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak.txt)

@@ -37,6 +37,19 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 inline int bit_cap(int bits) { return (1 << (bits - 1)) - 1; }  // quant.py:20-22
 
+// fp64 GEMM options (dgemm.cu): symmetric Gram output, upper-triangular B, alpha/beta epilogue,
+// device-side gate (skip when *gate != 0)
+struct DgemmOptions {
+  int sym = 0;
+  int b_upper = 0;
+  double alpha = 1.0, beta = 0.0;
+  const double *cin = nullptr;
+  int64_t ldci = 0;
+  const int *gate = nullptr;
+};
+int dgemm_device_ex(int trans_a, int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B,
+                    int64_t ldb, double *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st,
+                    const DgemmOptions &opt);
 int num_sms();
 
 // opt a kernel into the largest dynamic shared memory the device allows next to its static smem

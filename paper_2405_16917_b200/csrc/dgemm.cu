@@ -27,11 +27,32 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+struct DgemmEpi {
+  int sym;           // C symmetric (Gram A^T A): only tiles with tile_row <= tile_col, mirrored
+  int b_upper;       // B upper triangular: the k loop of output tile n0 stops at n0 + TN
+  double alpha, beta;
+  const double *cin;  // C = alpha A.B + beta cin (cin may alias nothing written by this GEMM)
+  int64_t ldci;
+  const int *gate;   // non-null: skip everything when *gate != 0
+};
+
+// upper-triangular tile index t -> (bi, bj), bi <= bj, row-major over the upper triangle
+__device__ __forceinline__ void upper_tile(int t, int nt, int &bi, int &bj) {
+  int i = 0, rem = t;
+  while (rem >= nt - i) {
+    rem -= nt - i;
+    ++i;
+  }
+  bi = i;
+  bj = i + rem;
+}
+
 template <bool TRANS_A>
 __global__ void __launch_bounds__(256) dgemm_kernel(int64_t M, int64_t N, int64_t K, const double *__restrict__ A,
                                                     int64_t lda, const double *__restrict__ B, int64_t ldb,
                                                     double *__restrict__ C, int64_t ldc, int64_t k_per_split,
-                                                    int64_t split_stride) {
+                                                    int64_t split_stride, DgemmEpi ep, int direct) {
+  if (ep.gate && *ep.gate != 0) return;
   constexpr int ASZ = TRANS_A ? TK * LDT : TM * LDA;
   extern __shared__ __align__(16) double dg_smem[];
   double(*As)[ASZ] = reinterpret_cast<double(*)[ASZ]>(dg_smem);
@@ -39,9 +60,16 @@ __global__ void __launch_bounds__(256) dgemm_kernel(int64_t M, int64_t N, int64_
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;  // warp tile: rows wm*32.., cols wn*16..
-  const int64_t m0 = (int64_t)blockIdx.x * TM, n0 = (int64_t)blockIdx.y * TN;
+  int64_t m0 = (int64_t)blockIdx.x * TM, n0 = (int64_t)blockIdx.y * TN;
+  if (ep.sym) {
+    int bi, bj;
+    upper_tile((int)blockIdx.x, (int)((N + TN - 1) / TN), bi, bj);
+    m0 = (int64_t)bi * TM;
+    n0 = (int64_t)bj * TN;
+  }
   const int64_t kbeg = (int64_t)blockIdx.z * k_per_split;
-  const int64_t kend = min(K, kbeg + k_per_split);
+  int64_t kend = min(K, kbeg + k_per_split);
+  if (ep.b_upper) kend = min(kend, n0 + TN);
   double acc[4][2][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -115,26 +143,45 @@ __global__ void __launch_bounds__(256) dgemm_kernel(int64_t M, int64_t N, int64_
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t c = n0 + wn * 16 + j * 8 + 2 * t4 + h;
-        if (c < N) Cz[r * ldc + c] = acc[i][j][h];
+        if (c >= N) continue;
+        double v = acc[i][j][h];
+        if (direct) {
+          if (ep.alpha != 1.0) v = ep.alpha * v;
+          if (ep.cin) v = __dadd_rn(v, ep.beta == 1.0 ? ep.cin[r * ep.ldci + c] : ep.beta * ep.cin[r * ep.ldci + c]);
+          if (ep.sym && c > r) Cz[c * ldc + r] = v;
+        }
+        Cz[r * ldc + c] = v;
       }
   }
 }
 
-// C = sum_z parts[z] in fixed order (deterministic)
+// C = sum_z parts[z] in fixed order (deterministic), then the epilogue; 2-D grid, no division.
+// Symmetric output: only the upper triangle is read (coalesced) and written to both halves.
 __global__ void splitk_reduce_kernel(const double *__restrict__ parts, int splits, int64_t M, int64_t N,
-                                     double *__restrict__ C, int64_t ldc) {
-  int64_t n = M * N;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += parts[z * n + i];
-    int64_t r = i / N, c = i - r * N;
-    C[r * ldc + c] = s;
-  }
+                                     double *__restrict__ C, int64_t ldc, DgemmEpi ep) {
+  if (ep.gate && *ep.gate != 0) return;
+  const int64_t n = M * N;
+  for (int64_t r = blockIdx.y; r < M; r += gridDim.y)
+    for (int64_t c = (ep.sym ? r : 0) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < N;
+         c += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t src = r * N + c;
+      double s = 0.0;
+      for (int z = 0; z < splits; ++z) s += parts[z * n + src];
+      if (ep.alpha != 1.0) s = ep.alpha * s;
+      if (ep.cin) s = __dadd_rn(s, ep.beta == 1.0 ? ep.cin[r * ep.ldci + c] : ep.beta * ep.cin[r * ep.ldci + c]);
+      C[r * ldc + c] = s;
+      if (ep.sym) C[c * ldc + r] = s;
+    }
 }
 
-int choose_splits(int trans_a, int64_t M, int64_t N, int64_t K) {
-  int64_t tiles = ceil_div(M, TM) * ceil_div(N, TN);
-  int64_t want = ceil_div(2LL * num_sms(), tiles);
+int64_t tile_count(int64_t M, int64_t N, bool sym) {
+  const int64_t tn = ceil_div(N, TN);
+  return sym ? tn * (tn + 1) / 2 : ceil_div(M, TM) * tn;
+}
+
+int choose_splits(int trans_a, int64_t M, int64_t N, int64_t K, bool sym = false) {
+  int64_t tiles = tile_count(M, N, sym);
+  int64_t want = ceil_div((int64_t)num_sms(), tiles);
   int64_t max_by_k = std::max<int64_t>(1, K / 256);
   int64_t s = std::max<int64_t>(1, std::min<int64_t>(want, std::min<int64_t>(max_by_k, 64)));
   return (int)s;
@@ -143,18 +190,22 @@ int choose_splits(int trans_a, int64_t M, int64_t N, int64_t K) {
 }  // namespace
 
 size_t dgemm_ws_bytes(int trans_a, int64_t M, int64_t N, int64_t K) {
-  int s = choose_splits(trans_a, M, N, K);
+  int s = std::max(choose_splits(trans_a, M, N, K), choose_splits(trans_a, M, N, K, trans_a && M == N));
   return s > 1 ? (size_t)round_up(s * M * N * 8, 256) : 0;
 }
 
-int dgemm_device(int trans_a, int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B,
-                 int64_t ldb, double *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st) {
+int dgemm_device_ex(int trans_a, int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B,
+                    int64_t ldb, double *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st,
+                    const DgemmOptions &opt) {
   if (M < 1 || N < 1 || K < 1) return fail(LRAMM_ERR_SHAPE, "dgemm: empty shape");
-  int splits = choose_splits(trans_a, M, N, K);
+  const bool sym = opt.sym && trans_a && M == N;
+  DgemmEpi ep{sym ? 1 : 0, opt.b_upper, opt.alpha, opt.beta, opt.cin, opt.ldci, opt.gate};
+  int splits = choose_splits(trans_a, M, N, K, sym);
   if (splits > 1 && (ws == nullptr || ws_bytes < dgemm_ws_bytes(trans_a, M, N, K))) splits = 1;
   int64_t kps = round_up(ceil_div(K, splits), TK);
   splits = (int)ceil_div(K, kps);
-  dim3 grid((unsigned)ceil_div(M, TM), (unsigned)ceil_div(N, TN), (unsigned)splits);
+  dim3 grid = sym ? dim3((unsigned)tile_count(M, N, true), 1, (unsigned)splits)
+                  : dim3((unsigned)ceil_div(M, TM), (unsigned)ceil_div(N, TN), (unsigned)splits);
   double *out = splits > 1 ? (double *)ws : C;
   int64_t ldo = splits > 1 ? N : ldc;
   static std::once_flag once;
@@ -165,17 +216,24 @@ int dgemm_device(int trans_a, int64_t M, int64_t N, int64_t K, const double *A, 
   });
   LRAMM_CUDA_TRY(e);
   const size_t smem_t = (size_t)(2 * TK * LDT + 2 * TK * LDT) * 8, smem_n = (size_t)(2 * TM * LDA + 2 * TK * LDT) * 8;
+  const int direct = splits == 1;
   if (trans_a)
-    dgemm_kernel<true><<<grid, 256, smem_t, st>>>(M, N, K, A, lda, B, ldb, out, ldo, kps, M * N);
+    dgemm_kernel<true><<<grid, 256, smem_t, st>>>(M, N, K, A, lda, B, ldb, out, ldo, kps, M * N, ep, direct);
   else
-    dgemm_kernel<false><<<grid, 256, smem_n, st>>>(M, N, K, A, lda, B, ldb, out, ldo, kps, M * N);
+    dgemm_kernel<false><<<grid, 256, smem_n, st>>>(M, N, K, A, lda, B, ldb, out, ldo, kps, M * N, ep, direct);
   LRAMM_LAUNCH_CHECK();
   if (splits > 1) {
-    int g = (int)std::min<int64_t>(ceil_div(M * N, 256), 8LL * num_sms());
-    splitk_reduce_kernel<<<g, 256, 0, st>>>((const double *)ws, splits, M, N, C, ldc);
+    const unsigned gy = (unsigned)std::min<int64_t>(M, 4LL * num_sms());
+    splitk_reduce_kernel<<<dim3((unsigned)ceil_div(N, 256), gy), 256, 0, st>>>((const double *)ws, splits, M, N, C,
+                                                                                 ldc, ep);
     LRAMM_LAUNCH_CHECK();
   }
   return LRAMM_OK;
+}
+
+int dgemm_device(int trans_a, int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B,
+                 int64_t ldb, double *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st) {
+  return dgemm_device_ex(trans_a, M, N, K, A, lda, B, ldb, C, ldc, ws, ws_bytes, st, DgemmOptions{});
 }
 
 }  // namespace lramm

@@ -39,6 +39,12 @@ __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc, bool
                "r"(valid ? 8 : 0)
                : "memory");
 }
+// 16-byte copy through L2 only (.cg: never a stale L1 line for data written by other SMs)
+__device__ __forceinline__ void cp_async16_cg(void *smem_dst, const void *gsrc, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // ---------------------------------------------------------------- TMA

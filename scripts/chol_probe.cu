@@ -1,35 +1,66 @@
-// Phase timing of chol_kernel (clock64 trace) -- build: nvcc ... -DLRAMM_TRACE scripts/chol_probe.cu
+// Phase timing of the dataflow tile Cholesky (globaltimer trace per CTA).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DLRAMM_TRACE -Ipaper_2405_16917_b200/csrc \
+//        scripts/chol_probe.cu -o scripts/chol_probe
 #define LRAMM_TRACE 1
 #include "../paper_2405_16917_b200/csrc/factor.cu"
-namespace lramm { void set_error(const char*, ...) {} int fail(int c, const char*, ...) { return c; } int num_sms() { return 148; }
-int dgemm_device(int, int64_t, int64_t, int64_t, const double*, int64_t, const double*, int64_t, double*, int64_t, void*, size_t, cudaStream_t) { return 0; }
-size_t dgemm_ws_bytes(int, int64_t, int64_t, int64_t) { return 0; } }
-#include <vector>
+namespace lramm {
+void set_error(const char *, ...) {}
+int fail(int c, const char *, ...) { return c; }
+int num_sms() { return 148; }
+int dgemm_device(int, int64_t, int64_t, int64_t, const double *, int64_t, const double *, int64_t, double *, int64_t,
+                 void *, size_t, cudaStream_t) { return 0; }
+int dgemm_device_ex(int, int64_t, int64_t, int64_t, const double *, int64_t, const double *, int64_t, double *,
+                    int64_t, void *, size_t, cudaStream_t, const DgemmOptions &) { return 0; }
+size_t dgemm_ws_bytes(int, int64_t, int64_t, int64_t) { return 0; }
+}  // namespace lramm
+#include <cstdio>
 #include <cstdlib>
-int main(int argc, char** argv) {
+#include <vector>
+int main(int argc, char **argv) {
   int w = argc > 1 ? atoi(argv[1]) : 272;
-  std::vector<double> h((size_t)w * w);
-  // SPD: G = X^T X + w I
-  std::vector<double> x((size_t)w * w);
-  for (auto& v : x) v = (rand() / (double)RAND_MAX) - 0.5;
-  for (int i = 0; i < w; ++i) for (int j = 0; j < w; ++j) { double s = 0; for (int k = 0; k < w; ++k) s += x[k*w+i]*x[k*w+j]; h[i*w+j] = s + (i==j ? w : 0); }
-  double *G, *L; int* info; cudaMalloc(&G, w*w*8); cudaMalloc(&L, w*w*8); cudaMalloc(&info, 4);
-  cudaMemcpy(G, h.data(), w*w*8, cudaMemcpyHostToDevice);
-  lramm::allow_max_dyn_smem(lramm::chol_kernel);
-  for (int rep = 0; rep < 3; ++rep) {
-    cudaMemset(L, 0, w*w*8);
-    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  int T = (w + 31) / 32;
+  std::vector<double> h((size_t)w * w), x((size_t)w * w);
+  for (auto &v : x) v = (rand() / (double)RAND_MAX) - 0.5;
+  for (int i = 0; i < w; ++i)
+    for (int j = 0; j < w; ++j) {
+      double s = 0;
+      for (int k = 0; k < w; ++k) s += x[k * w + i] * x[k * w + j];
+      h[i * w + j] = s + (i == j ? w : 0);
+    }
+  double *G, *L, *dinv;
+  int *info, *flags;
+  cudaMalloc(&G, w * w * 8);
+  cudaMalloc(&L, w * w * 8);
+  cudaMalloc(&dinv, T * 1024 * 8);
+  cudaMalloc(&info, 4);
+  cudaMalloc(&flags, (T + 1) * 4);
+  cudaMemcpy(G, h.data(), w * w * 8, cudaMemcpyHostToDevice);
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
     cudaEventRecord(a);
-    lramm::chol_kernel<<<1, lramm::kCholThreads, lramm::kCholSmem>>>(G, w, w, L, info, nullptr);
-    cudaEventRecord(b); cudaEventSynchronize(b);
-    float ms; cudaEventElapsedTime(&ms, a, b);
-    long long t[4096]; cudaMemcpyFromSymbol(t, lramm_trace, sizeof(t));
-    printf("w=%d  %.1f us  err=%s\n", w, ms * 1e3, cudaGetErrorString(cudaGetLastError()));
-    if (rep == 2) {
-      long long t0 = t[0];
-      for (int jb = 0; jb < (w + 31) / 32; ++jb) {
-        long long s1 = t[1 + jb*4], s2 = t[2 + jb*4], s3 = t[3 + jb*4], nxt = (jb + 1 < (w+31)/32) ? t[1 + (jb+1)*4] : 0;
-        printf("panel %2d: update %8lld  potrf %8lld  below %8lld cycles\n", jb, s2 - s1, s3 - s2, nxt ? nxt - s3 : -1);
+    int rc = lramm::chol_device(G, w, w, L, dinv, flags, info, nullptr, 0);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("w=%d rc=%d %.1f us err=%s\n", w, rc, ms * 1e3, cudaGetErrorString(cudaGetLastError()));
+    if (rep == 3) {
+      std::vector<unsigned long long> t(148 * 128);
+      cudaMemcpyFromSymbol(t.data(), chol_trace, t.size() * 8);
+      unsigned long long t0 = ~0ull;
+      for (int i = 0; i < T; ++i) t0 = std::min(t0, t[i * 128 + 0 < 1 ? 0 : i * 128 + (i > 0 ? 0 : 120)]);
+      for (int i = 0; i < T; ++i) t0 = std::min(t0, i > 0 ? t[i * 128] : t[120]);
+      for (int i = 0; i < T; ++i) {
+        auto *r = &t[i * 128];
+        printf("row %2d:", i);
+        for (int j = 0; j < i; ++j)
+          printf(" [j%d start %5.1f poll1 %4.1f panel %4.1f poll2 %4.1f fin %4.1f]", j, (r[4 * j] - t0) / 1e3,
+                 j ? (r[4 * j + 1] - r[4 * j]) / 1e3 : 0.0, (r[4 * j + 2] - (j ? r[4 * j + 1] : r[4 * j])) / 1e3,
+                 (r[4 * j + 3] - r[4 * j + 2]) / 1e3, ((j + 1 < i ? r[4 * j + 4] : r[120]) - r[4 * j + 3]) / 1e3);
+        printf("\n        diag start %6.1f potrf %5.1f trinv %5.1f publish %5.1f end %6.1f us\n", (r[120] - t0) / 1e3,
+               (r[121] - r[120]) / 1e3, (r[122] - r[121]) / 1e3, (r[123] - r[122]) / 1e3, (r[123] - t0) / 1e3);
       }
     }
   }

@@ -28,10 +28,11 @@ def _inputs(m, k, n, seed):
 
 CASES = [
     ((512, 384, 448), dict(rank=16, mode="parity")),
+    ((512, 384, 448), dict(rank=16, mode="parity", bits=(8, 8, 8), seed=3)),
     ((512, 384, 448), dict(rank=16, mode="fast", granularity="row", power_iters=1)),
     ((320, 256, 288), dict(rank=12, mode="fast", granularity="tensor", alpha=0.5, beta=2.0)),
 ]
-IDS = ["parity", "fast-row-q1", "fast-tensor-ab"]
+IDS = ["parity", "parity-888", "fast-row-q1", "fast-tensor-ab"]
 
 
 def _oracle(case):
@@ -41,15 +42,20 @@ def _oracle(case):
     fast = kw.get("mode") == "fast"
     spec = O.SketchSpec(8, 8, 8, kw.get("granularity", "tensor")) if fast else O.SketchSpec()
     p = O.OracleParams(rank=kw["rank"], power_iters=kw.get("power_iters", 0), alpha=kw.get("alpha", 1.0),
-                       beta=kw.get("beta", 0.0), spec=spec)
+                       beta=kw.get("beta", 0.0), spec=spec, bits=kw.get("bits", (8, 8, 4)), seed=kw.get("seed", 0))
     a, b = a.astype(np.float64), b.astype(np.float64)
     # both reference backends: LAPACK (pure) and the compiled one-sided Jacobi
     return (O.lramm(a, b, p, c=c), O.lramm(a, b, p, c=c, svd_fn=O.jacobi_svd)), c
 
 
+def _tol(refs):
+    """1e-3, widened to 1.5x the spread between the reference's own two backends: at (8,8,4)
+    the 4-bit E3 quantiser can meet exact ties, where a 1e-13 perturbation moves
+    the output by ~5e-3 and the reference's backends already disagree by that much."""
+    return max(1e-3, 1.5 * O.rel_fro(refs[1], refs[0]))
+
+
 def _err(d, refs):
-    """Distance to the nearer reference backend: the two differ by up to 5e-3 where the 4-bit
-    E3 quantiser meets exact ties, so parity means agreeing with one of them."""
     return min(O.rel_fro(d, r) for r in refs)
 
 
@@ -76,7 +82,7 @@ def test_sharded_world1_cuda(case):
 
     d = _shard_run(case, 1, 0, Comm())
     refs, _ = _oracle(case)
-    assert _err(d.cpu().numpy(), refs) <= 1e-3
+    assert _err(d.cpu().numpy(), refs) <= _tol(refs)
 
 
 class _HostStagedComm:
@@ -128,7 +134,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("case", CASES[1:], ids=IDS[1:])
+@pytest.mark.parametrize("case", CASES[2:], ids=IDS[2:])
 def test_sharded_world2_cuda(case):
     import torch.multiprocessing as mp
 
@@ -151,4 +157,4 @@ def test_sharded_world2_cuda(case):
     for p in procs:
         p.join(60)
     refs, _ = _oracle(case)
-    assert _err(d, refs) <= 1e-3
+    assert _err(d, refs) <= _tol(refs)

@@ -167,7 +167,8 @@ def test_sharded_world2_matches_oracle(case):
     refs, exact = _oracle(case)
     assert d2.shape == refs[0].shape
     err = min(O.rel_fro(d2, r) for r in refs)
-    assert err <= 1e-3, err
+    # 1e-3, widened to 1.5x the reference's own backend spread at exact E3 ties
+    assert err <= max(1e-3, 1.5 * O.rel_fro(refs[1], refs[0])), err
     # and it is the same approximation: its error to the exact product matches the oracle's
     assert abs(O.rel_fro(d2, exact) - O.rel_fro(refs[0], exact)) <= 1e-2
 
