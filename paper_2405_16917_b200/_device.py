@@ -85,6 +85,7 @@ class OmegaCache:
         self.capacity = capacity
         self.host: OrderedDict = OrderedDict()
         self.dev: OrderedDict = OrderedDict()
+        self._pins: dict = {}
 
     def host_omega(self, seed: int, ncols: int, width: int) -> np.ndarray:
         key = (int(seed), int(ncols), int(width))
@@ -93,9 +94,15 @@ class OmegaCache:
             entropy = [int(seed) & 0xFFFFFFFFFFFFFFFF, 0x534B, int(ncols), int(width)]
             g = np.random.Generator(np.random.Philox(np.random.SeedSequence(entropy)))
             om = np.ascontiguousarray(g.standard_normal((ncols, width)))
+            if torch.cuda.is_available():  # page-locked: the host API's upload is an async DMA
+                pinned = torch.empty(om.shape, dtype=torch.float64, pin_memory=True)
+                pinned.numpy()[...] = om
+                om = pinned.numpy()
+                self._pins[key] = pinned
             self.host[key] = om
             if len(self.host) > self.capacity:
-                self.host.popitem(last=False)
+                old, _ = self.host.popitem(last=False)
+                self._pins.pop(old, None)
         else:
             self.host.move_to_end(key)
         return om

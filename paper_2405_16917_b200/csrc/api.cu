@@ -70,7 +70,7 @@ int rsvd_device(const void *, int, int64_t, int64_t, const lramm_params_t &, con
 size_t lramm_ws_bytes(int64_t, int64_t, int64_t, const lramm_params_t &, int);
 int lramm_device(const void *, const void *, int, int64_t, int64_t, int64_t, const lramm_params_t &, const double *,
                  const double *, const void *, int, void *, int, int *, void *, size_t, lramm_timings_t *,
-                 cudaStream_t);
+                 cudaStream_t, cudaEvent_t b_ready = nullptr);
 
 // ---------------------------------------------------------------- host-side device memory
 // One cached device arena + stream for the host-pointer entry points (grow-only,
@@ -80,6 +80,8 @@ struct HostCtx {
   char *buf = nullptr;
   size_t cap = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t copy = nullptr;  // second upload stream (B, Omega_B, C) so A's chain starts first
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   int *status = nullptr;
   int dev = -1;
 };
@@ -94,10 +96,15 @@ static int host_reserve(HostCtx &c, size_t bytes) {
     c.buf = nullptr;
     c.cap = 0;
     c.st = nullptr;
+    c.copy = nullptr;
+    c.ev_a = c.ev_b = nullptr;
     c.status = nullptr;
     c.dev = dev;
   }
   if (!c.st) LRAMM_CUDA_TRY(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
+  if (!c.copy) LRAMM_CUDA_TRY(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+  if (!c.ev_a) LRAMM_CUDA_TRY(cudaEventCreateWithFlags(&c.ev_a, cudaEventDisableTiming));
+  if (!c.ev_b) LRAMM_CUDA_TRY(cudaEventCreateWithFlags(&c.ev_b, cudaEventDisableTiming));
   if (!c.status) LRAMM_CUDA_TRY(cudaMalloc(&c.status, 64));
   if (bytes > c.cap) {
     if (c.buf) LRAMM_CUDA_TRY(cudaFree(c.buf));
@@ -388,13 +395,20 @@ int lramm_host_lramm(const void *a, const void *b, int in_dtype, int64_t m, int6
   char *dd = ar.take<char>(m * n * ds);
   char *dc = cmat ? ar.take<char>(m * n * cs) : nullptr;
   void *w = ar.take<char>((int64_t)ws);
-  LRAMM_CUDA_TRY(cudaMemcpyAsync(da, a, m * k * es, cudaMemcpyHostToDevice, c.st));
-  LRAMM_CUDA_TRY(cudaMemcpyAsync(db, b, k * n * es, cudaMemcpyHostToDevice, c.st));
+  // uploads overlap the factorisation: A and Omega_A on the compute stream (A's chain starts as
+  // soon as they land), then B, Omega_B (and C) on the copy stream behind them; B's chain
+  // waits only for its own operands (b_ready)
   LRAMM_CUDA_TRY(cudaMemcpyAsync(oa, omega_a, k * wa * 8, cudaMemcpyHostToDevice, c.st));
-  LRAMM_CUDA_TRY(cudaMemcpyAsync(ob, omega_b, n * wb * 8, cudaMemcpyHostToDevice, c.st));
-  if (cmat) LRAMM_CUDA_TRY(cudaMemcpyAsync(dc, cmat, m * n * cs, cudaMemcpyHostToDevice, c.st));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(da, a, m * k * es, cudaMemcpyHostToDevice, c.st));
+  LRAMM_CUDA_TRY(cudaEventRecord(c.ev_a, c.st));
+  LRAMM_CUDA_TRY(cudaStreamWaitEvent(c.copy, c.ev_a, 0));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(ob, omega_b, n * wb * 8, cudaMemcpyHostToDevice, c.copy));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(db, b, k * n * es, cudaMemcpyHostToDevice, c.copy));
+  if (cmat) LRAMM_CUDA_TRY(cudaMemcpyAsync(dc, cmat, m * n * cs, cudaMemcpyHostToDevice, c.copy));
+  LRAMM_CUDA_TRY(cudaEventRecord(c.ev_b, c.copy));
+  if (timings) LRAMM_CUDA_TRY(cudaStreamWaitEvent(c.st, c.ev_b, 0));  // stage timings stay comparable
   LRAMM_TRY(lramm_device(da, db, in_dtype, m, k, n, *params, oa, ob, dc, c_dtype, dd, d_dtype, c.status, w, ws,
-                         timings, c.st));
+                         timings, c.st, c.ev_b));
   LRAMM_CUDA_TRY(cudaMemcpyAsync(d, dd, m * n * ds, cudaMemcpyDeviceToHost, c.st));
   return finish(c);
 }

@@ -389,7 +389,8 @@ size_t lramm_ws_bytes(int64_t m, int64_t k, int64_t n, const lramm_params_t &P, 
 
 int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t k, int64_t n, const lramm_params_t &P,
                  const double *omega_a, const double *omega_b, const void *c, int c_dtype, void *d, int d_dtype,
-                 int *status, void *ws, size_t ws_bytes, lramm_timings_t *timings, cudaStream_t st) {
+                 int *status, void *ws, size_t ws_bytes, lramm_timings_t *timings, cudaStream_t st,
+                 cudaEvent_t b_ready) {
   LRAMM_TRY(validate_params(P, true));
   if (P.rank < 2) return fail(LRAMM_ERR_PARAM, "rank must be >= 2, got %d", P.rank);
   if (in_dtype != LRAMM_F32 && in_dtype != LRAMM_F64) return fail(LRAMM_ERR_PARAM, "inputs must be F32 or F64");
@@ -426,6 +427,7 @@ int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t 
   SideStream &side = side_stream(st);
   LRAMM_CUDA_TRY(cudaEventRecord(side.fork, st));
   LRAMM_CUDA_TRY(cudaStreamWaitEvent(side.st, side.fork, 0));
+  if (b_ready) LRAMM_CUDA_TRY(cudaStreamWaitEvent(side.st, b_ready, 0));  // B (and C) uploaded on another stream
   LRAMM_TRY(run_rsvd(b, in_dtype, L.rb, P, omega_b, L.UB, r, L.SB, L.VB, r, side.st));
   LRAMM_TRY(run_rsvd(a, in_dtype, L.ra, P, omega_a, L.UA, r, L.SA, L.VA, r, st));
   LRAMM_CUDA_TRY(cudaEventRecord(side.join, side.st));
