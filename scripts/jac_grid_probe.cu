@@ -47,14 +47,13 @@ int main(int argc, char **argv) {
   }
   std::vector<unsigned long long> t(148 * 128);
   cudaMemcpyFromSymbol(t.data(), chol_trace, t.size() * 8);
-  double steps = 0, send = 0, recv = 0;
+  double ph[4] = {0, 0, 0, 0};
   int cnt = 0;
   for (int g = 0; g < 2000 && (g + 1) * 4 < (int)t.size(); ++g) {
-    if (!t[g * 4] || !t[g * 4 + 1] || !t[g * 4 + 2] || !t[(g + 1) * 4]) continue;
-    steps += (t[g * 4 + 1] - t[g * 4]) / 1e3;
-    send += (t[g * 4 + 2] - t[g * 4 + 1]) / 1e3;
-    recv += (t[(g + 1) * 4] - t[g * 4 + 2]) / 1e3;
+    if (!t[g * 4] || !t[g * 4 + 1] || !t[g * 4 + 2] || !t[g * 4 + 3] || !t[(g + 1) * 4]) continue;
+    for (int q = 0; q < 4; ++q) ph[q] += ((q < 3 ? t[g * 4 + q + 1] : t[(g + 1) * 4]) - t[g * 4 + q]) / 1e3;
     ++cnt;
   }
-  printf("rounds sampled %d: avg steps %.2f us, send %.2f us, receive %.2f us\n", cnt, steps / cnt, send / cnt, recv / cnt);
+  printf("rounds %d: phase us (grid kernel: steps/send/recv/-; gram kernel: gram/steps/apply/exchange): "
+         "%.2f %.2f %.2f %.2f\n", cnt, ph[0] / cnt, ph[1] / cnt, ph[2] / cnt, ph[3] / cnt);
 }
