@@ -523,6 +523,13 @@ def run_sharded(args, cfg, world, rank, local):
     return 0
 
 
+# dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full` captures
+# (profiles/r01_ncu_jacobi_c2.txt)
+NCU_DRAM_BYTES = {
+    "jacobi_cluster_kernel<9, false>": 639488,
+}
+
+
 def dominant_roofline(name, us, cfg, peaks):
     """Algorithmic work of the dominant kernel per launch over its measured time."""
     if not us:
@@ -531,12 +538,17 @@ def dominant_roofline(name, us, cfg, peaks):
     w = r + cfg["oversample"]
     fp64_peak = 36.7  # TFLOP/s, DFMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak.txt)
     if "jacobi" in name:
-        # one-sided Jacobi on w x w: ~ sweeps * w(w-1)/2 pairs * 6w flops; sweeps measured ~11
-        flops = 11 * (w * (w - 1) / 2) * 6 * w
+        # one-sided Jacobi on the w x w R^T: sweeps x w(w-1)/2 pairs x 8w flops (dot product 2w +
+        # rotation 6w); sweeps measured by scripts/sweeps_probe.py: 9 (c1-c3), 10 (c5)
+        sweeps = 10 if w > 1000 else 9
+        flops = sweeps * (w * (w - 1) / 2) * 8 * w
         achieved = flops / (us * 1e-6) / 1e12
+        traffic = next((v for k, v in NCU_DRAM_BYTES.items() if k in name), None)
         return {"bound": "tensor", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak, "traffic": None,
-                "peak_source": "measured fp64 DFMA peak (not in MEASURED_PEAKS.json); kernel is latency-bound"}
+                "frac": achieved / fp64_peak, "traffic": traffic, "algorithmic_flops": flops,
+                "peak_source": "measured fp64 DFMA/DMMA peak (profiles/r01_fp64_peak.txt; not in MEASURED_PEAKS.json)",
+                "note": "latency-bound sequential rotation chain (w steps per sweep); traffic: columns stay in "
+                        "shared memory, DRAM bytes are the one-time load of R^T"}
     if "chol" in name or "trinv" in name:
         flops = w ** 3 / 3.0
         achieved = flops / (us * 1e-6) / 1e12
