@@ -159,6 +159,20 @@ int lramm_scale_round_clip(const double *a, int64_t rows, int64_t cols, int64_t 
 int lramm_igemm(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, const int8_t *b,
                 int64_t ldb, const lramm_epilogue_t *epi, int split_k, lramm_stream_t stream);
 
+/* Bit budgets 9..24 (quant.py:16-28 allows [2, 24]): a quantised int32 operand is carried as
+ * 1..4 planes of 8-bit limbs, v = sum_l limb_l 256^l (unsigned low limbs, signed top limb).
+ * lramm_split_limbs: rows x cols int32 (ld lds) -> nlimb planes of rows x ldd int8 (plane
+ * stride rows * ldd bytes, ldd a multiple of 16).  lramm_igemm_limbs: C = A . B^T over limb
+ * planes (pa / pb bytes between planes), the la x lb int8 tensor-core products accumulated
+ * exactly in int64 (acc64: M x N scratch), then the lramm_igemm epilogue (out_dtype F32/F64
+ * dequantised, or I64 for the raw exact product).  Replaces the int64 imatmul of
+ * _core.pyx:35-50 for operands beyond +-127. */
+int lramm_split_limbs(const int32_t *src, int64_t rows, int64_t cols, int64_t lds, int nlimb, int8_t *dst,
+                      int64_t ldd, lramm_stream_t stream);
+int lramm_igemm_limbs(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, int64_t pa, int la,
+                      const int8_t *b, int64_t ldb, int64_t pb, int lb, int64_t *acc64, const lramm_epilogue_t *epi,
+                      lramm_stream_t stream);
+
 /* fp64 GEMM.  trans_a = 0: C(MxN) = A(MxK) . B(KxN); trans_a = 1: C = A^T . B with
  * A stored K x M (split-K over the long dimension, deterministic reduction).
  * All row-major.  ws >= lramm_dgemm_ws(trans_a, M, N, K). */

@@ -68,6 +68,11 @@ size_t rsvd_ws_bytes(int64_t, int64_t, const lramm_params_t &, int);
 int rsvd_device(const void *, int, int64_t, int64_t, const lramm_params_t &, const double *, double *, double *,
                 double *, int *, void *, size_t, cudaStream_t);
 size_t lramm_ws_bytes(int64_t, int64_t, int64_t, const lramm_params_t &, int);
+int igemm_limbs_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, int64_t pa, int la,
+                       const int8_t *b, int64_t ldb, int64_t pb, int lb, int64_t *acc64,
+                       const lramm_epilogue_t &epi, cudaStream_t st);
+int split_limbs_device(const int32_t *src, int64_t rows, int64_t cols, int64_t lds, int nlimb, int8_t *dst,
+                       int64_t ldd, cudaStream_t st);
 int lramm_device(const void *, const void *, int, int64_t, int64_t, int64_t, const lramm_params_t &, const double *,
                  const double *, const void *, int, void *, int, int *, void *, size_t, lramm_timings_t *,
                  cudaStream_t, cudaEvent_t b_ready = nullptr);
@@ -178,6 +183,21 @@ int lramm_igemm(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, c
   return igemm_device(M, N, K, a, lda, b, ldb, *epi, split_k, (cudaStream_t)stream);
 }
 
+int lramm_split_limbs(const int32_t *src, int64_t rows, int64_t cols, int64_t lds, int nlimb, int8_t *dst,
+                      int64_t ldd, lramm_stream_t stream) {
+  if (nlimb < 1 || nlimb > 4) return fail(LRAMM_ERR_PARAM, "split_limbs: 1..4 limbs");
+  if (rows < 1 || cols < 1 || ldd < cols || (ldd % 16)) return fail(LRAMM_ERR_SHAPE, "split_limbs: bad shape");
+  return split_limbs_device(src, rows, cols, lds, nlimb, dst, ldd, (cudaStream_t)stream);
+}
+
+int lramm_igemm_limbs(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, int64_t pa, int la,
+                      const int8_t *b, int64_t ldb, int64_t pb, int lb, int64_t *acc64, const lramm_epilogue_t *epi,
+                      lramm_stream_t stream) {
+  if (!epi) return fail(LRAMM_ERR_PARAM, "igemm_limbs: epilogue is NULL");
+  if (!acc64) return fail(LRAMM_ERR_PARAM, "igemm_limbs: acc64 is NULL");
+  return igemm_limbs_device(M, N, K, a, lda, pa, la, b, ldb, pb, lb, acc64, *epi, (cudaStream_t)stream);
+}
+
 int lramm_dgemm(int trans_a, int64_t M, int64_t N, int64_t K, const double *a, int64_t lda, const double *b,
                 int64_t ldb, double *c, int64_t ldc, void *ws, size_t ws_bytes, lramm_stream_t stream) {
   return dgemm_device(trans_a, M, N, K, a, lda, b, ldb, c, ldc, ws, ws_bytes, (cudaStream_t)stream);
@@ -266,22 +286,16 @@ int lramm_host_matmul(const double *a, const double *b, double *out, int64_t m, 
 }
 
 namespace {
-__global__ void i32_to_i8_kernel(const int32_t *__restrict__ x, int64_t rows, int64_t cols, int transpose,
-                                 int8_t *__restrict__ y, int64_t ldy, int *bad) {
-  int64_t n = rows * cols;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i / cols, c = i - r * cols;
-    int v = x[i];
-    if (v < -127 || v > 127) *bad = 1;
-    if (transpose)
-      y[c * ldy + r] = (int8_t)v;
-    else
-      y[r * ldy + c] = (int8_t)v;
-  }
-}
-__global__ void i32_to_i64_kernel(const int32_t *__restrict__ x, int64_t n, int64_t *__restrict__ y) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = x[i];
+// out (cols x rows) = x^T through 32 x 32 tiles
+__global__ void transpose_i32_kernel(const int32_t *__restrict__ x, int64_t rows, int64_t cols,
+                                     int32_t *__restrict__ out) {
+  __shared__ int32_t t[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8)
+    if (r0 + i < rows && c0 + threadIdx.x < cols) t[i][threadIdx.x] = x[(r0 + i) * cols + c0 + threadIdx.x];
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8)
+    if (c0 + i < cols && r0 + threadIdx.x < rows) out[(c0 + i) * rows + r0 + threadIdx.x] = t[threadIdx.x][i];
 }
 __global__ void max_abs_i32_kernel(const int32_t *x, int64_t n, unsigned *out) {
   unsigned m = 0;
@@ -296,40 +310,42 @@ __global__ void max_abs_i32_kernel(const int32_t *x, int64_t n, unsigned *out) {
 
 // exact int32 x int32 -> int64 for |entries| <= 127 (bit budgets <= 8) on the int8 tensor cores
 int lramm_host_imatmul(const int32_t *a, const int32_t *b, int64_t *out, int64_t m, int64_t k, int64_t n) {
+  // exact int64 product of arbitrary int32 matrices (_core.pyx:35-50): each operand is split
+  // into 1..4 8-bit limbs (as many as its largest magnitude needs) and the limb products run
+  // on the int8 tensor cores, accumulated exactly in int64
   if (m < 1 || k < 1 || n < 1) return fail(LRAMM_ERR_SHAPE, "inner dimensions differ");
   HostCtx &c = host_ctx();
   std::lock_guard<std::mutex> g(c.mu);
   const int64_t ldk = round_up(k, 16);
-  size_t need = (size_t)round_up((m * k + k * n) * 4, 256) + round_up((m + n) * ldk, 256) + round_up(m * n * 4, 256) +
-                round_up(m * n * 8, 256) + 8192;
+  size_t need = (size_t)round_up((m * k + 2 * k * n) * 4, 256) + round_up(4 * (m + n) * ldk, 256) +
+                round_up(2 * m * n * 8, 256) + 8192;
   LRAMM_TRY(host_reserve(c, need));
   Arena ar(c.buf, c.cap);
-  int32_t *da = ar.take<int32_t>(m * k), *db = ar.take<int32_t>(k * n);
-  int8_t *qa = ar.take<int8_t>(m * ldk), *qb = ar.take<int8_t>(n * ldk);
-  int32_t *acc = ar.take<int32_t>(m * n);
-  int64_t *o64 = ar.take<int64_t>(m * n);
-  int *bad = ar.take<int>(4);
+  int32_t *da = ar.take<int32_t>(m * k), *db = ar.take<int32_t>(k * n), *dbt = ar.take<int32_t>(n * k);
+  int8_t *qa = ar.take<int8_t>(4 * m * ldk), *qb = ar.take<int8_t>(4 * n * ldk);
+  int64_t *acc = ar.take<int64_t>(m * n), *o64 = ar.take<int64_t>(m * n);
+  unsigned *mx = ar.take<unsigned>(4);
   LRAMM_CUDA_TRY(cudaMemcpyAsync(da, a, m * k * 4, cudaMemcpyHostToDevice, c.st));
   LRAMM_CUDA_TRY(cudaMemcpyAsync(db, b, k * n * 4, cudaMemcpyHostToDevice, c.st));
-  LRAMM_CUDA_TRY(cudaMemsetAsync(bad, 0, 16, c.st));
-  LRAMM_CUDA_TRY(cudaMemsetAsync(qa, 0, m * ldk, c.st));
-  LRAMM_CUDA_TRY(cudaMemsetAsync(qb, 0, n * ldk, c.st));
-  int grid = 4 * num_sms();
-  i32_to_i8_kernel<<<grid, 256, 0, c.st>>>(da, m, k, 0, qa, ldk, bad);
-  i32_to_i8_kernel<<<grid, 256, 0, c.st>>>(db, k, n, 1, qb, ldk, bad);  // B^T: n x k
+  LRAMM_CUDA_TRY(cudaMemsetAsync(mx, 0, 16, c.st));
+  const int grid = 4 * num_sms();
+  max_abs_i32_kernel<<<grid, 256, 0, c.st>>>(da, m * k, mx);
+  max_abs_i32_kernel<<<grid, 256, 0, c.st>>>(db, k * n, mx + 1);
+  transpose_i32_kernel<<<dim3((unsigned)ceil_div(n, 32), (unsigned)ceil_div(k, 32)), dim3(32, 8), 0, c.st>>>(
+      db, k, n, dbt);  // B^T: n x k, K-major
   LRAMM_LAUNCH_CHECK();
-  int hbad = 0;
-  LRAMM_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, c.st));
+  unsigned hmx[2] = {0, 0};
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(hmx, mx, 8, cudaMemcpyDeviceToHost, c.st));
   LRAMM_CUDA_TRY(cudaStreamSynchronize(c.st));
-  if (hbad) return fail(LRAMM_ERR_UNSUPPORTED, "imatmul: entries beyond +-127 need the multi-limb path");
-  if ((double)k * 127.0 * 127.0 >= 2147483648.0) return fail(LRAMM_ERR_OVERFLOW, "imatmul: k too large for int32");
+  auto limbs = [](unsigned v) { return v <= 127u ? 1 : (v <= 32767u ? 2 : (v <= 8388607u ? 3 : 4)); };
+  const int la = limbs(hmx[0]), lb = limbs(hmx[1]);
+  LRAMM_TRY(split_limbs_device(da, m, k, k, la, qa, ldk, c.st));
+  LRAMM_TRY(split_limbs_device(dbt, n, k, k, lb, qb, ldk, c.st));
   lramm_epilogue_t e = {};
-  e.out_dtype = LRAMM_I32;
-  e.out = acc;
+  e.out_dtype = LRAMM_I64;
+  e.out = o64;
   e.ldo = n;
-  LRAMM_TRY(igemm_device(m, n, k, qa, ldk, qb, ldk, e, 1, c.st));
-  i32_to_i64_kernel<<<grid, 256, 0, c.st>>>(acc, m * n, o64);
-  LRAMM_LAUNCH_CHECK();
+  LRAMM_TRY(igemm_limbs_device(m, n, k, qa, ldk, m * ldk, la, qb, ldk, n * ldk, lb, acc, e, c.st));
   LRAMM_CUDA_TRY(cudaMemcpyAsync(out, o64, m * n * 8, cudaMemcpyDeviceToHost, c.st));
   LRAMM_CUDA_TRY(cudaMemsetAsync(c.status, 0, 4, c.st));
   return finish(c);

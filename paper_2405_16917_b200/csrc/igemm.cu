@@ -31,6 +31,8 @@ struct EpiDev {
   double alpha, beta;
   const void *c;
   int64_t ldc;
+  int shift;  // EK_I64_ADD: out += acc * 2^shift (limb-pair products of multi-limb operands)
+  int signs;  // bit 0: A int8 signed, bit 1: B int8 signed (unsigned limbs otherwise)
 };
 
 // Correctly rounded a / s for |a| < 2^53 integer-valued a and normal s > 0, given y = RN(1/s):
@@ -65,10 +67,11 @@ __device__ __forceinline__ double div_exact(double a, double s, double y) {
 }
 
 // reference dequantisation + alpha/beta on one accumulator (bit-exact IEEE fp64)
-__device__ __forceinline__ double epi_value(const EpiDev &e, int32_t acc, int64_t row, int64_t col) {
+template <typename AccT>
+__device__ __forceinline__ double epi_value(const EpiDev &e, AccT acc, int64_t row, int64_t col) {
   double rs = e.row_scale ? e.row_scale[row * e.row_scale_inc] : 1.0;
   double cs = e.col_scale ? e.col_scale[col * e.col_scale_inc] : 1.0;
-  double v = __ddiv_rn((double)acc, __dmul_rn(rs, cs));  // acc.astype(f64) / (sa*sb)
+  double v = __ddiv_rn((double)acc, __dmul_rn(rs, cs));  // acc.astype(f64) / (sa*sb) (int64: RN convert)
   if (e.beta != 0.0 && e.c != nullptr) {
     double cv = e.c_dtype == LRAMM_F32 ? (double)((const float *)e.c)[row * e.ldc + col]
                                        : ((const double *)e.c)[row * e.ldc + col];
@@ -114,7 +117,7 @@ constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 constexpr int kSmemBudget = 200 * 1024;
 
 // epilogue kinds (compile time): raw int32 store / atomic add, or dequantised f32 / f64
-enum { EK_I32 = 0, EK_I32_ATOMIC = 1, EK_F32 = 2, EK_F64 = 3 };
+enum { EK_I32 = 0, EK_I32_ATOMIC = 1, EK_F32 = 2, EK_F64 = 3, EK_I64_ADD = 4 };
 
 template <int EK, bool TRANS, bool AB>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -170,7 +173,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = sm100::idesc_i8(BM, BN);
+      const uint32_t idesc = (sm100::idesc_i8(BM, BN) & ~((1u << 7) | (1u << 10))) | ((uint32_t)(epi.signs & 1) << 7) |
+                             ((uint32_t)((epi.signs >> 1) & 1) << 10);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % stages;
         const uint32_t ph = (uint32_t)(i / stages) & 1u;
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // epilogue warps 2..9: TMEM -> registers (thread = row; the two warps of a TMEM lane quarter
     // take alternate 16-column halves) -> dequant -> shared tile (32-column chunks in the drained
     // pipeline buffers) -> coalesced stores (warp = rows, lanes = columns)
-    constexpr bool RAW = EK == EK_I32 || EK == EK_I32_ATOMIC;
+    constexpr bool RAW = EK == EK_I32 || EK == EK_I32_ATOMIC || EK == EK_I64_ADD;
     const int ew = warp - 2;               // 0..7
     const int quarter = warp & 3;          // TMEM lane quarter (hardware: warp id mod 4)
     const int half = ew >> 2;              // column half of each 32-column chunk
@@ -247,6 +251,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               ((int32_t *)epi.out)[idx] = itile[rr * 33 + lane];
             } else if constexpr (EK == EK_I32_ATOMIC) {
               atomicAdd((int32_t *)epi.out + idx, itile[rr * 33 + lane]);
+            } else if constexpr (EK == EK_I64_ADD) {
+              ((int64_t *)epi.out)[idx] += (int64_t)itile[rr * 33 + lane] * ((int64_t)1 << epi.shift);
             } else {
               double v = tile[rr * 33 + lane];
               if constexpr (AB) v = epi_alpha_beta(epi, v, grow, gcol);
@@ -268,6 +274,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               ((int32_t *)epi.out)[idx] = itile[rr * 33 + jj];
             } else if constexpr (EK == EK_I32_ATOMIC) {
               atomicAdd((int32_t *)epi.out + idx, itile[rr * 33 + jj]);
+            } else if constexpr (EK == EK_I64_ADD) {
+              ((int64_t *)epi.out)[idx] += (int64_t)itile[rr * 33 + jj] * ((int64_t)1 << epi.shift);
             } else {
               double v = tile[rr * 33 + jj];
               if constexpr (AB) v = epi_alpha_beta(epi, v, grow, gcol);
@@ -292,6 +300,45 @@ __global__ void epilogue_kernel(const int32_t *__restrict__ acc, int64_t M, int6
     int64_t r = i / N, c = i - r * N;
     epi_store(epi, acc[r * lda + c], r, c);
   }
+}
+
+// epilogue over an exact int64 accumulator (multi-limb products): float output only, or the
+// raw int64 (imatmul)
+__global__ void epilogue64_kernel(const int64_t *__restrict__ acc, int64_t M, int64_t N, int64_t lda, EpiDev e) {
+  for (int64_t r = blockIdx.y; r < M; r += gridDim.y)
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < N; c += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t a = acc[r * lda + c];
+      const int64_t idx = e.transpose_out ? c * e.ldo + r : r * e.ldo + c;
+      if (e.out_dtype == LRAMM_I64) {
+        ((int64_t *)e.out)[idx] = a;
+        continue;
+      }
+      const double v = epi_value(e, a, r, c);
+      if (e.out_dtype == LRAMM_F64)
+        ((double *)e.out)[idx] = v;
+      else
+        ((float *)e.out)[idx] = __double2float_rn(v);
+    }
+}
+
+// 8-bit limb planes of int32 values (K-major rows x ld): v = sum_l limb_l 256^l with unsigned low
+// limbs and a signed top limb (floor division), L = 2 for |v| < 2^15, 3 for |v| < 2^23
+__global__ void split_limbs_kernel(const int32_t *__restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+                                   int nlimb, int8_t *__restrict__ dst, int64_t ldd, int64_t plane) {
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ldd; c += (int64_t)gridDim.x * blockDim.x) {
+      int32_t v = c < cols ? src[r * lds + c] : 0;
+      for (int l = 0; l < nlimb; ++l) {
+        int8_t d;
+        if (l == nlimb - 1) {
+          d = (int8_t)v;  // |v| <= 127 here by construction
+        } else {
+          d = (int8_t)(uint8_t)(v & 0xFF);
+          v = v >> 8;  // arithmetic shift = floor division by 256
+        }
+        dst[l * plane + r * ldd + c] = d;
+      }
+    }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -337,10 +384,17 @@ EpiDev to_dev(const lramm_epilogue_t &e) {
   d.beta = e.beta;
   d.c = e.c;
   d.ldc = e.ldc;
+  d.shift = 0;
+  d.signs = 3;
   return d;
 }
 
 }  // namespace
+
+// limb-pair launch parameters (set only around igemm_limbs_device's launches; thread-local so
+// concurrent host threads do not interfere)
+static thread_local int g_limb_shift = 0;
+static thread_local int g_limb_signs = 3;
 
 // BN: multiple of 16 in [16, 256] covering N with the fewest tiles and least padding
 int pick_bn(int64_t N) {
@@ -370,9 +424,11 @@ int igemm_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, 
   CUtensorMap ta, tb;
   LRAMM_TRY(make_tmap_i8(&ta, a, M, K, lda, BM));
   LRAMM_TRY(make_tmap_i8(&tb, b, N, K, ldb, BN));
-  const int ek = epi.out_dtype == LRAMM_I32 ? (epi.accumulate ? EK_I32_ATOMIC : EK_I32)
-                                            : (epi.out_dtype == LRAMM_F64 ? EK_F64 : EK_F32);
-  const bool ab = ek >= EK_F32 && (epi.alpha != 1.0 || (epi.beta != 0.0 && epi.c != nullptr));
+  const int ek = epi.out_dtype == LRAMM_I64 ? EK_I64_ADD
+                 : epi.out_dtype == LRAMM_I32 ? (epi.accumulate ? EK_I32_ATOMIC : EK_I32)
+                                              : (epi.out_dtype == LRAMM_F64 ? EK_F64 : EK_F32);
+  if (ek == EK_I64_ADD && split_k > 1) return fail(LRAMM_ERR_PARAM, "igemm: int64 accumulation runs without split-K");
+  const bool ab = (ek == EK_F32 || ek == EK_F64) && (epi.alpha != 1.0 || (epi.beta != 0.0 && epi.c != nullptr));
   using KernT = void (*)(CUtensorMap, CUtensorMap, int64_t, int64_t, int64_t, int, int, int, EpiDev);
   KernT kern = nullptr;
 #define LRAMM_IG_PICK(EKV, TR, ABV) \
@@ -383,11 +439,56 @@ int igemm_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, 
   LRAMM_IG_PICK(EK_F32, false, true) LRAMM_IG_PICK(EK_F32, true, true)
   LRAMM_IG_PICK(EK_F64, false, false) LRAMM_IG_PICK(EK_F64, true, false)
   LRAMM_IG_PICK(EK_F64, false, true) LRAMM_IG_PICK(EK_F64, true, true)
+  LRAMM_IG_PICK(EK_I64_ADD, false, false)
 #undef LRAMM_IG_PICK
   if (!kern) return fail(LRAMM_ERR_PARAM, "igemm: unsupported epilogue");
   LRAMM_CUDA_TRY(allow_max_dyn_smem(kern));
   dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(N, BN), (unsigned)split_k);
-  kern<<<grid, kThreads, smem, st>>>(ta, tb, M, N, K, BN, stages, kb_per, to_dev(epi));
+  EpiDev ed = to_dev(epi);
+  ed.shift = g_limb_shift;
+  ed.signs = g_limb_signs;
+  kern<<<grid, kThreads, smem, st>>>(ta, tb, M, N, K, BN, stages, kb_per, ed);
+  LRAMM_LAUNCH_CHECK();
+  return LRAMM_OK;
+}
+
+// C = dequant(A . B^T) for multi-limb operands: A has la limb planes (rows x lda each, plane
+// stride pa bytes), B lb planes; the la x lb int8 products accumulate exactly into acc64
+// (int64, M x N) with the shifts 8(i + j), then the fp64 dequant epilogue (or raw int64 out)
+int igemm_limbs_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, int64_t pa, int la,
+                       const int8_t *b, int64_t ldb, int64_t pb, int lb, int64_t *acc64,
+                       const lramm_epilogue_t &epi, cudaStream_t st) {
+  if (la < 1 || lb < 1 || la > 4 || lb > 4) return fail(LRAMM_ERR_PARAM, "igemm_limbs: 1..4 limbs per operand");
+  LRAMM_CUDA_TRY(cudaMemsetAsync(acc64, 0, (size_t)M * N * sizeof(int64_t), st));
+  lramm_epilogue_t e = {};
+  e.out_dtype = LRAMM_I64;
+  e.out = acc64;
+  e.ldo = N;
+  // each limb product accumulates exactly in int32 while K * 255^2 < 2^31: longer K in chunks
+  const int64_t kc = 33024;  // multiple of 128, 33024 * 255^2 < 2^31
+  for (int64_t k0 = 0; k0 < K; k0 += kc) {
+    const int64_t kk = std::min(kc, K - k0);
+    for (int i = 0; i < la; ++i)
+      for (int j = 0; j < lb; ++j) {
+        g_limb_shift = 8 * (i + j);
+        g_limb_signs = (i == la - 1 ? 1 : 0) | (j == lb - 1 ? 2 : 0);
+        const int rc = igemm_device(M, N, kk, a + i * pa + k0, lda, b + j * pb + k0, ldb, e, 1, st);
+        g_limb_shift = 0;
+        g_limb_signs = 3;
+        if (rc) return rc;
+      }
+  }
+  const unsigned gy = (unsigned)std::min<int64_t>(M, 8LL * num_sms());
+  epilogue64_kernel<<<dim3((unsigned)ceil_div(N, 256), gy), 256, 0, st>>>(acc64, M, N, N, to_dev(epi));
+  LRAMM_LAUNCH_CHECK();
+  return LRAMM_OK;
+}
+
+int split_limbs_device(const int32_t *src, int64_t rows, int64_t cols, int64_t lds, int nlimb, int8_t *dst,
+                       int64_t ldd, cudaStream_t st) {
+  const unsigned gy = (unsigned)std::min<int64_t>(rows, 8LL * num_sms());
+  split_limbs_kernel<<<dim3((unsigned)ceil_div(ldd, 256), gy), 256, 0, st>>>(src, rows, cols, lds, nlimb, dst, ldd,
+                                                                             rows * ldd);
   LRAMM_LAUNCH_CHECK();
   return LRAMM_OK;
 }

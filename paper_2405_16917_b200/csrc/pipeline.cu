@@ -23,6 +23,11 @@ int quantize_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int6
                     int transpose, void *q, int q_dtype, int64_t ldq, double *scales, int *nonfinite, void *ws,
                     size_t ws_bytes, cudaStream_t st);
 size_t quantize_ws_bytes(int64_t rows, int64_t cols);
+int igemm_limbs_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, int64_t pa, int la,
+                       const int8_t *b, int64_t ldb, int64_t pb, int lb, int64_t *acc64,
+                       const lramm_epilogue_t &epi, cudaStream_t st);
+int split_limbs_device(const int32_t *src, int64_t rows, int64_t cols, int64_t lds, int nlimb, int8_t *dst,
+                       int64_t ldd, cudaStream_t st);
 int igemm_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, const int8_t *b, int64_t ldb,
                  const lramm_epilogue_t &epi, int split_k, cudaStream_t st);
 int epilogue_device(const int32_t *acc, int64_t M, int64_t N, int64_t lda, const lramm_epilogue_t &epi,
@@ -70,12 +75,18 @@ __global__ void summarize_status_kernel(const int *jac_info, int njac, const int
 
 inline int elem_grid(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 8LL * num_sms())); }
 
-struct QOp {  // a quantised K-major operand
+struct QOp {  // a quantised K-major operand (bit budgets > 8: `limbs` 8-bit planes, see split_limbs)
   int8_t *q = nullptr;
   int64_t ld = 0;
   double *scale = nullptr;
   int64_t inc = 0;
+  int limbs = 1;
+  int64_t plane = 0;  // bytes between limb planes
+  int64_t rows = 0;
 };
+
+// 8-bit limbs needed for a bit budget: 1 (<= 8, the plain signed int8), 2 (<= 16), 3 (<= 24)
+inline int limbs_for(int bits) { return bits <= 8 ? 1 : (bits <= 16 ? 2 : 3); }
 
 struct RsvdBufs {
   int64_t rows = 0, cols = 0, w = 0, r = 0;
@@ -93,10 +104,13 @@ struct RsvdBufs {
   size_t qr_bytes = 0, svd_bytes = 0, gemm_bytes = 0, qz_bytes = 0;
 };
 
-QOp take_qop(Arena &ar, int64_t rows, int64_t kdim, int64_t nscale) {
+QOp take_qop(Arena &ar, int64_t rows, int64_t kdim, int64_t nscale, int limbs = 1) {
   QOp o;
   o.ld = round_up(kdim, 16);
-  o.q = ar.take<int8_t>(rows * o.ld);
+  o.limbs = limbs;
+  o.rows = rows;
+  o.plane = rows * o.ld;
+  o.q = ar.take<int8_t>(rows * o.ld * limbs);
   o.scale = ar.take<double>(nscale);
   o.inc = nscale > 1 ? 1 : 0;
   return o;
@@ -151,7 +165,7 @@ RsvdBufs carve_rsvd(Arena &ar, int64_t rows, int64_t cols, int x_dtype, const lr
 
 // C (M x N fp64) = dequant(A . B^T): row scales of A, column scales of B
 int qprod(const QOp &A, const QOp &B, int64_t M, int64_t N, int64_t K, double *C, int64_t ldc, int transpose_out,
-          int32_t *acc, cudaStream_t st) {
+          int32_t *acc, cudaStream_t st, int64_t *acc64 = nullptr) {
   lramm_epilogue_t e = {};
   e.out_dtype = LRAMM_F64;
   e.transpose_out = transpose_out;
@@ -163,6 +177,10 @@ int qprod(const QOp &A, const QOp &B, int64_t M, int64_t N, int64_t K, double *C
   e.col_scale_inc = B.inc;
   e.alpha = 1.0;
   e.beta = 0.0;
+  if (A.limbs > 1 || B.limbs > 1) {
+    if (!acc64) return fail(LRAMM_ERR_WORKSPACE, "qprod: multi-limb product needs an int64 accumulator");
+    return igemm_limbs_device(M, N, K, A.q, A.ld, A.plane, A.limbs, B.q, B.ld, B.plane, B.limbs, acc64, e, st);
+  }
   const int64_t tiles = ceil_div(M, 128) * ceil_div(N, pick_bn(N));
   const int64_t kb = ceil_div(K, 128);
   int split = 1;
@@ -179,15 +197,32 @@ int qprod(const QOp &A, const QOp &B, int64_t M, int64_t N, int64_t K, double *C
 }
 
 int quant(const void *x, int dtype, int64_t rows, int64_t cols, int64_t ldx, int bits, int gran, int transpose,
-          QOp &o, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st) {
-  return quantize_device(x, dtype, rows, cols, ldx, bits, gran, transpose, o.q, LRAMM_I8, o.ld, o.scale, nonfinite,
-                         ws, ws_bytes, st);
+          QOp &o, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st, int32_t *tmp32 = nullptr) {
+  if (o.limbs <= 1)
+    return quantize_device(x, dtype, rows, cols, ldx, bits, gran, transpose, o.q, LRAMM_I8, o.ld, o.scale, nonfinite,
+                           ws, ws_bytes, st);
+  // bit budgets > 8: the reference's integers (int32, bit-exact) -> 8-bit limb planes
+  if (!tmp32) return fail(LRAMM_ERR_WORKSPACE, "quant: multi-limb operand needs an int32 staging buffer");
+  const int64_t orows = transpose ? cols : rows, kdim = transpose ? rows : cols;
+  LRAMM_TRY(quantize_device(x, dtype, rows, cols, ldx, bits, gran, transpose, tmp32, LRAMM_I32, o.ld, o.scale,
+                            nonfinite, ws, ws_bytes, st));
+  return split_limbs_device(tmp32, orows, kdim, o.ld, o.limbs, o.q, o.ld, st);
 }
 
-int check_bits_dev(int bits, const char *what) {
+int check_bits_dev(int bits, const char *what, bool limbs_ok = false) {
   if (bits < 2 || bits > 24) return fail(LRAMM_ERR_PARAM, "%s must be an integer in [2, 24], got %d", what, bits);
-  if (bits > 8)
-    return fail(LRAMM_ERR_UNSUPPORTED, "%s = %d: the int8 tensor-core path supports bit budgets <= 8", what, bits);
+  if (bits > 8 && !limbs_ok)
+    return fail(LRAMM_ERR_UNSUPPORTED, "%s = %d: the fast-mode sketch products support bit budgets <= 8", what, bits);
+  return LRAMM_OK;
+}
+
+// recombination guard: the reference's int64 rule (quant.py:87-93) for multi-limb products (their
+// int64 accumulation is exact), the int32 rule for single int8 products
+int check_acc(int64_t K, int bits_a, int bits_b);
+int check_acc_qm(int64_t K, int bits) {
+  if (bits <= 8) return check_acc(K, bits, bits);
+  if ((long double)K * bit_cap(bits) * bit_cap(bits) >= 9223372036854775808.0L)
+    return fail(LRAMM_ERR_OVERFLOW, "k=%lld with bit budgets (%d, %d) risks int64 overflow", (long long)K, bits, bits);
   return LRAMM_OK;
 }
 
@@ -275,7 +310,7 @@ int validate_params(const lramm_params_t &P, bool need_bits) {
     if (P.power_iters > 0) LRAMM_TRY(check_bits_dev(P.power_bits, "power_bits"));
   }
   if (need_bits)
-    for (int i = 0; i < 3; ++i) LRAMM_TRY(check_bits_dev(P.bits[i], "bits"));
+    for (int i = 0; i < 3; ++i) LRAMM_TRY(check_bits_dev(P.bits[i], "bits", true));  // > 8: int8 limbs
   return LRAMM_OK;
 }
 
@@ -284,6 +319,8 @@ struct LrammBufs {
   double *UA, *SA, *VA, *UB, *SB, *VB, *E1, *Zsc, *E2T, *Usc;
   QOp vt, wq, e1q, zq, e2q, uq;
   int32_t *e1acc;
+  int32_t *tmp32 = nullptr;  // int32 quantiser staging (bit budgets > 8)
+  int64_t *acc64 = nullptr;  // exact int64 accumulator of multi-limb products
   int *nonfinite, *jinfo;
   void *qws;
   size_t qbytes;
@@ -304,12 +341,22 @@ LrammBufs carve_lramm(Arena &ar, int64_t m, int64_t k, int64_t n, int in_dtype, 
   L.Zsc = ar.take<double>(n * r);
   L.E2T = ar.take<double>(n * r);
   L.Usc = ar.take<double>(m * r);
-  L.vt = take_qop(ar, r, k, 1);
-  L.wq = take_qop(ar, r, k, 1);
-  L.e1q = take_qop(ar, r, r, 1);
-  L.zq = take_qop(ar, n, r, 1);
-  L.e2q = take_qop(ar, n, r, 1);
-  L.uq = take_qop(ar, m, r, 1);
+  const int l1 = limbs_for(P.bits[0]), l2 = limbs_for(P.bits[1]), l3 = limbs_for(P.bits[2]);
+  L.vt = take_qop(ar, r, k, 1, l1);
+  L.wq = take_qop(ar, r, k, 1, l1);
+  L.e1q = take_qop(ar, r, r, 1, l2);
+  L.zq = take_qop(ar, n, r, 1, l2);
+  L.e2q = take_qop(ar, n, r, 1, l3);
+  L.uq = take_qop(ar, m, r, 1, l3);
+  if (l1 > 1 || l2 > 1 || l3 > 1) {
+    const int64_t mx = std::max(std::max(m, n), k);
+    L.tmp32 = ar.take<int32_t>(mx * round_up(std::max(k, r), 16));
+    int64_t acc_elems = 0;
+    if (l1 > 1) acc_elems = std::max(acc_elems, r * r);
+    if (l2 > 1) acc_elems = std::max(acc_elems, r * n);
+    if (l3 > 1) acc_elems = std::max(acc_elems, m * n);
+    L.acc64 = ar.take<int64_t>(acc_elems);
+  }
   L.e1acc = ar.take<int32_t>(r * r);
   L.nonfinite = ar.take<int>(4);
   L.jinfo = ar.take<int>(4);
@@ -401,9 +448,9 @@ int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t 
                 (long long)std::min(k, n));
   const int64_t r = P.rank;
   const int d1 = P.bits[0], d2 = P.bits[1], d3 = P.bits[2];
-  LRAMM_TRY(check_acc(k, d1, d1));
-  LRAMM_TRY(check_acc(r, d2, d2));
-  LRAMM_TRY(check_acc(r, d3, d3));
+  LRAMM_TRY(check_acc_qm(k, d1));
+  LRAMM_TRY(check_acc_qm(r, d2));
+  LRAMM_TRY(check_acc_qm(r, d3));
   if (P.mode == LRAMM_MODE_FAST) {
     int64_t mx = std::max(std::max(m, n), k);
     LRAMM_TRY(check_acc(mx, P.sketch_bits, P.sketch_bits));
@@ -441,18 +488,18 @@ int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t 
   LRAMM_TRY(mark(2));
   LRAMM_CUDA_TRY(cudaMemsetAsync(L.nonfinite, 0, 4 * sizeof(int), st));
   // ---- E1 = QM(V_A^T U_B, d1)   (r x r, K = k)
-  LRAMM_TRY(quant(L.VA, LRAMM_F64, k, r, r, d1, LRAMM_GRAN_TENSOR, 1, L.vt, L.nonfinite, L.qws, L.qbytes, st));
-  LRAMM_TRY(quant(L.UB, LRAMM_F64, k, r, r, d1, LRAMM_GRAN_TENSOR, 1, L.wq, L.nonfinite, L.qws, L.qbytes, st));
-  LRAMM_TRY(qprod(L.vt, L.wq, r, r, k, L.E1, r, 0, L.e1acc, st));
+  LRAMM_TRY(quant(L.VA, LRAMM_F64, k, r, r, d1, LRAMM_GRAN_TENSOR, 1, L.vt, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
+  LRAMM_TRY(quant(L.UB, LRAMM_F64, k, r, r, d1, LRAMM_GRAN_TENSOR, 1, L.wq, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
+  LRAMM_TRY(qprod(L.vt, L.wq, r, r, k, L.E1, r, 0, L.e1acc, st, L.acc64));
   LRAMM_TRY(mark(3));
   // ---- E2 = QM(E1 Zsc, d2)   (r x n, K = r) stored transposed for E3
-  LRAMM_TRY(quant(L.E1, LRAMM_F64, r, r, r, d2, LRAMM_GRAN_TENSOR, 0, L.e1q, L.nonfinite, L.qws, L.qbytes, st));
-  LRAMM_TRY(quant(L.Zsc, LRAMM_F64, n, r, r, d2, LRAMM_GRAN_TENSOR, 0, L.zq, L.nonfinite, L.qws, L.qbytes, st));
-  LRAMM_TRY(qprod(L.e1q, L.zq, r, n, r, L.E2T, r, 1, nullptr, st));
+  LRAMM_TRY(quant(L.E1, LRAMM_F64, r, r, r, d2, LRAMM_GRAN_TENSOR, 0, L.e1q, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
+  LRAMM_TRY(quant(L.Zsc, LRAMM_F64, n, r, r, d2, LRAMM_GRAN_TENSOR, 0, L.zq, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
+  LRAMM_TRY(qprod(L.e1q, L.zq, r, n, r, L.E2T, r, 1, nullptr, st, L.acc64));
   LRAMM_TRY(mark(4));
   // ---- E3 = QM(Usc E2, d3) ; D = alpha E3 + beta C   (m x n, K = r)
-  LRAMM_TRY(quant(L.Usc, LRAMM_F64, m, r, r, d3, LRAMM_GRAN_TENSOR, 0, L.uq, L.nonfinite, L.qws, L.qbytes, st));
-  LRAMM_TRY(quant(L.E2T, LRAMM_F64, n, r, r, d3, LRAMM_GRAN_TENSOR, 0, L.e2q, L.nonfinite, L.qws, L.qbytes, st));
+  LRAMM_TRY(quant(L.Usc, LRAMM_F64, m, r, r, d3, LRAMM_GRAN_TENSOR, 0, L.uq, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
+  LRAMM_TRY(quant(L.E2T, LRAMM_F64, n, r, r, d3, LRAMM_GRAN_TENSOR, 0, L.e2q, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
   {
     lramm_epilogue_t e = {};
     e.out_dtype = d_dtype;
@@ -467,7 +514,11 @@ int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t 
     e.c = c;
     e.c_dtype = c_dtype;
     e.ldc = n;
-    LRAMM_TRY(igemm_device(m, n, r, L.uq.q, L.uq.ld, L.e2q.q, L.e2q.ld, e, 1, st));
+    if (L.uq.limbs > 1)
+      LRAMM_TRY(igemm_limbs_device(m, n, r, L.uq.q, L.uq.ld, L.uq.plane, L.uq.limbs, L.e2q.q, L.e2q.ld, L.e2q.plane,
+                                   L.e2q.limbs, L.acc64, e, st));
+    else
+      LRAMM_TRY(igemm_device(m, n, r, L.uq.q, L.uq.ld, L.e2q.q, L.e2q.ld, e, 1, st));
   }
   LRAMM_TRY(mark(5));
   gather_info_kernel<<<1, 32, 0, st>>>(L.ra.info, L.rb.info, L.ra.compl_st, L.rb.compl_st, L.ra.nonfinite,

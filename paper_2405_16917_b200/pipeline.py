@@ -22,9 +22,8 @@ import torch
 from . import _native as N
 from ._device import OMEGA, WORKSPACE, dtype_code, ptr, require_device, stream_handle, to_device_matrix
 from .errors import ParameterError, ShapeError
-from .quant import MMA_BITS_MAX, _check_bits
+from .quant import _check_bits
 from .rsvd import DEFAULT_OVERSAMPLE, native_params, sketch_width
-from .errors import UnsupportedError
 
 _SEED_TAG_A = 0xA0
 _SEED_TAG_B = 0xB0
@@ -177,9 +176,6 @@ def _validate(a, b, params, c):
             raise ShapeError(f"c has shape {sc}, expected {(m, n)}")
     if params.rank > min(m, k) or params.rank > min(k, n):
         raise ParameterError(f"rank {params.rank} exceeds operand min dims {min(m, k)}, {min(k, n)}")
-    for d in params.bits:
-        if d > MMA_BITS_MAX:
-            raise UnsupportedError(f"bit budget {d}: the int8 tensor-core path supports bit budgets <= {MMA_BITS_MAX}")
     return m, k, n
 
 

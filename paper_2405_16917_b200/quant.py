@@ -5,7 +5,8 @@ Same public surface and semantics as the reference's `quant.py`
 scale = (2^(bits-1)-1) / max|a| in fp64, rint half-to-even, clamp, sentinel
 scale 1.0 for all-zero input, dequantisation acc / (sa*sb).  Integer data and
 scales are bit-identical to the reference's; products run as int8 tcgen05 GEMMs
-(bit budgets <= 8) with int32 accumulation.
+with int32 accumulation (bit budgets <= 8), or, for budgets 9..24 and long K, as
+8-bit limb products accumulated exactly in int64 (the reference's int64 imatmul).
 
 Inputs may be NumPy arrays (results come back as NumPy, the reference's types)
 or CUDA tensors (results stay on the device).
@@ -21,11 +22,16 @@ import torch
 
 from . import _native as N
 from ._device import WORKSPACE, dtype_code, ptr, require_device, stream_handle, to_device_matrix
-from .errors import OverflowRiskError, ParameterError, ShapeError, UnsupportedError
+from .errors import OverflowRiskError, ParameterError, ShapeError
 
 BITS_MIN = 2
 BITS_MAX = 24
-MMA_BITS_MAX = 8  # int8 tensor-core operands
+MMA_BITS_MAX = 8  # single int8 tensor-core operand; larger budgets use 8-bit limbs
+
+
+def limbs_for(bits):
+    """8-bit limb planes carrying a `bits`-wide integer (1 up to 8 bits, 2 up to 16, 3 up to 24)."""
+    return 1 if bits <= 8 else (2 if bits <= 16 else 3)
 
 
 def bit_cap(bits):
@@ -124,18 +130,10 @@ def dequantize(q):
 
 
 def _check_overflow(k, bits_a, bits_b):
-    # quant.py:87-93: worst-case |sum| = k * cap_a * cap_b must stay below 2^63
+    # quant.py:87-93: worst-case |sum| = k * cap_a * cap_b must stay below 2^63 (the device path
+    # accumulates exactly in int64 whenever int32 would not be enough)
     if k * bit_cap(bits_a) * bit_cap(bits_b) >= 1 << 63:
         raise OverflowRiskError(f"k={k} with bit budgets ({bits_a}, {bits_b}) risks int64 overflow")
-    # the tensor-core path accumulates in int32
-    if k * bit_cap(min(bits_a, MMA_BITS_MAX)) * bit_cap(min(bits_b, MMA_BITS_MAX)) >= 1 << 31:
-        raise OverflowRiskError(f"k={k} with bit budgets ({bits_a}, {bits_b}) risks int32 accumulator overflow")
-
-
-def _require_mma_bits(*bits):
-    for b in bits:
-        if b > MMA_BITS_MAX:
-            raise UnsupportedError(f"bit budget {b}: the int8 tensor-core path supports bit budgets <= {MMA_BITS_MAX}")
 
 
 def integer_matmul(qa, qb):
@@ -143,7 +141,6 @@ def integer_matmul(qa, qb):
     if qa.cols != qb.rows:
         raise ShapeError(f"inner dimensions differ: {tuple(qa.data.shape)} @ {tuple(qb.data.shape)}")
     _check_overflow(qa.cols, qa.bits, qb.bits)
-    _require_mma_bits(qa.bits, qb.bits)
     from . import kernels
 
     a = qa.data.cpu().numpy() if _is_cuda(qa.data) else qa.data
@@ -158,8 +155,20 @@ def qgemm_device(a: torch.Tensor, b: torch.Tensor, bits_a: int, bits_b: int, alp
     dev = a.device
     m, k = a.shape
     n = b.shape[1]
-    qa, sa, fa = quantize_device(a, bits_a, N.GRAN_TENSOR, False, N.I8)
-    qb, sb, fb = quantize_device(b, bits_b, N.GRAN_TENSOR, True, N.I8)  # B^T: n x k, K-major
+    la, lb = limbs_for(bits_a), limbs_for(bits_b)
+    single = la == 1 and lb == 1 and k * bit_cap(bits_a) * bit_cap(bits_b) < (1 << 31)
+    if single:
+        qa, sa, fa = quantize_device(a, bits_a, N.GRAN_TENSOR, False, N.I8)
+        qb, sb, fb = quantize_device(b, bits_b, N.GRAN_TENSOR, True, N.I8)  # B^T: n x k, K-major
+    else:  # reference integers (int32) -> 8-bit limb planes, exact int64 accumulation
+        ldk = ((k + 15) // 16) * 16
+        qa32, sa, fa = quantize_device(a, bits_a, N.GRAN_TENSOR, False, N.I32, ld=ldk)
+        qb32, sb, fb = quantize_device(b, bits_b, N.GRAN_TENSOR, True, N.I32, ld=ldk)
+        qa = torch.empty((la, m, ldk), dtype=torch.int8, device=dev)
+        qb = torch.empty((lb, n, ldk), dtype=torch.int8, device=dev)
+        st = stream_handle(dev)
+        N.check(N.LIB.lramm_split_limbs(ptr(qa32), m, k, ldk, la, ptr(qa), ldk, st))
+        N.check(N.LIB.lramm_split_limbs(ptr(qb32), n, k, ldk, lb, ptr(qb), ldk, st))
     out = torch.empty((m, n), dtype=out_dtype, device=dev)
     e = N.Epilogue()
     e.out_dtype = N.F64 if out_dtype == torch.float64 else N.F32
@@ -175,8 +184,13 @@ def qgemm_device(a: torch.Tensor, b: torch.Tensor, bits_a: int, bits_b: int, alp
         e.c = c.data_ptr()
         e.c_dtype = dtype_code(c)
         e.ldc = c.stride(0)
-    N.check(N.LIB.lramm_igemm(m, n, k, ptr(qa), qa.stride(0), ptr(qb), qb.stride(0), ctypes.byref(e), 1,
-                              stream_handle(dev)))
+    if single:
+        N.check(N.LIB.lramm_igemm(m, n, k, ptr(qa), qa.stride(0), ptr(qb), qb.stride(0), ctypes.byref(e), 1,
+                                  stream_handle(dev)))
+    else:
+        acc64 = torch.empty((m, n), dtype=torch.int64, device=dev)
+        N.check(N.LIB.lramm_igemm_limbs(m, n, k, ptr(qa), qa.stride(1), qa.stride(0), la, ptr(qb), qb.stride(1),
+                                        qb.stride(0), lb, ptr(acc64), ctypes.byref(e), stream_handle(dev)))
     if int(fa.item()) or int(fb.item()):
         raise ParameterError("cannot quantize non-finite entries")
     return out
@@ -195,7 +209,6 @@ def qgemm(a, b, bits_a, bits_b, alpha=1.0, beta=0.0, c=None):
     bits_a = _check_bits(bits_a, "bits_a")
     bits_b = _check_bits(bits_b, "bits_b")
     _check_overflow(sa_shape[1], bits_a, bits_b)
-    _require_mma_bits(bits_a, bits_b)
     on_dev = _is_cuda(a)
     dev = require_device(a.device if on_dev else None)
     ta = to_device_matrix(a, dev)

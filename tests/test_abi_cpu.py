@@ -78,8 +78,8 @@ def test_shape_errors_raise_before_device():
         L.lramm(a, a, L.LrammParams(rank=20))
     with pytest.raises(L.ShapeError):
         L.lramm(a, a, L.LrammParams(rank=2), c=np.ones((3, 3)))
-    with pytest.raises(L.UnsupportedError):
-        L.lramm(a, a, L.LrammParams(rank=2, bits=(16, 8, 8)))
+    with pytest.raises(L.ParameterError):
+        L.lramm(a, a, L.LrammParams(rank=2, bits=(25, 8, 8)))
 
 
 def test_no_cpu_fallback_without_device():

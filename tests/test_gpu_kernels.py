@@ -119,6 +119,18 @@ def test_imatmul_exact(mnk):
     assert np.array_equal(out, a.astype(np.int64) @ b.astype(np.int64))
 
 
+@pytest.mark.parametrize("amp,k", [(255, 64), (40000, 500), (1 << 20, 1000), ((1 << 31) - 1, 2)])
+def test_imatmul_multi_limb_exact(amp, k):
+    """Entries beyond +-127: limb decomposition, exact int64 like _core.imatmul."""
+    from paper_2405_16917_b200 import kernels
+
+    rng = np.random.Generator(np.random.Philox(key=amp % 1000))
+    a = rng.integers(-amp, amp, size=(33, k), endpoint=True).astype(np.int32)
+    b = rng.integers(-amp, amp, size=(k, 45), endpoint=True).astype(np.int32)
+    out = kernels.imatmul(a, b)
+    assert np.array_equal(out, a.astype(np.int64) @ b.astype(np.int64))
+
+
 def test_imatmul_extremes_and_shape_error():
     from paper_2405_16917_b200 import kernels
 
@@ -178,8 +190,24 @@ def test_qgemm_errors(L):
         L.qgemm(np.ones((2, 3)), np.ones((2, 3)), 8, 8)
     with pytest.raises(L.OverflowRiskError):
         L.qgemm(np.ones((1, (1 << 17) + 1)), np.ones(((1 << 17) + 1, 1)), 24, 24)
-    with pytest.raises(L.UnsupportedError):
-        L.qgemm(np.ones((2, 3)), np.ones((3, 2)), 16, 16)
+
+
+@pytest.mark.parametrize("bits", [(12, 12), (16, 16), (24, 24), (16, 8), (24, 12), (9, 3)])
+def test_qgemm_bitwise_limbs(L, bits):
+    """Bit budgets 9..24 (quant.py:16-28): 8-bit limb products, exact int64 accumulation."""
+    a = O.generate(37, 300, "normal", 60 + bits[0])
+    b = O.generate(300, 29, "uniform", 70 + bits[1])
+    assert np.array_equal(L.qgemm(a, b, *bits), O.qgemm(a, b, *bits))
+    c = O.generate(37, 29, "normal", 5)
+    assert np.array_equal(L.qgemm(a, b, *bits, alpha=1.5, beta=-2.0, c=c), O.qgemm(a, b, *bits, 1.5, -2.0, c))
+
+
+def test_qgemm_long_k_exact(L):
+    """K * 127^2 >= 2^31: the single int8 product would overflow int32; the limb path chunks K."""
+    k = 140000
+    a = O.generate(3, k, "normal", 1)
+    b = O.generate(k, 2, "normal", 2)
+    assert np.array_equal(L.qgemm(a, b, 8, 8), O.qgemm(a, b, 8, 8))
 
 
 def test_integer_matmul_and_dequantize(L):

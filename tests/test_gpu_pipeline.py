@@ -183,6 +183,26 @@ def test_lramm_device_tensors_and_fp32_output(L):
     assert d32.dtype == np.float32 and np.array_equal(d32, d_host.astype(np.float32))
 
 
+@pytest.mark.parametrize("bits", [(16, 16, 16), (24, 12, 8), (8, 8, 16)])
+def test_lramm_high_bit_budgets(L, bits):
+    """Bit budgets 9..24 in the recombination (test_pipeline.py:28-41 uses 16/24): limb products."""
+    a = O.synth(200, 160, "exp:12", 3, 0, 0)
+    b = O.synth(160, 180, "exp:12", 3, 0, 1)
+    kw = dict(rank=12, bits=bits, power_iters=1, oversample=6, seed=9)
+    d, _ = L.lramm(a, b, L.LrammParams(**kw))
+    ref = O.lramm(a, b, O.OracleParams(**kw))
+    ref2 = O.lramm(a, b, O.OracleParams(**kw), svd_fn=O.jacobi_svd)
+    assert min(O.rel_fro(d, ref), O.rel_fro(d, ref2)) <= max(1e-3, 1.5 * O.rel_fro(ref2, ref))
+    # and the recombination itself is bit-exact given the same factors (L2 gate, limb products)
+    fa = O.rsvd(a, 12, 1, 6, O.child_seeds(9)[0])
+    fb = O.rsvd(b, 12, 1, 6, O.child_seeds(9)[1])
+    e = O.recombine(fa, fb, bits)
+    e1 = L.qgemm(np.ascontiguousarray(fa.v.T), fb.u, bits[0], bits[0])
+    e2 = L.qgemm(e1, np.ascontiguousarray((fb.v * fb.sigma).T), bits[1], bits[1])
+    e3 = L.qgemm(np.ascontiguousarray(fa.u * fa.sigma), e2, bits[2], bits[2])
+    assert np.array_equal(e3, e)
+
+
 def test_lramm_nonfinite_input_raises(L):
     a = np.ones((20, 20))
     a[3, 4] = np.nan
