@@ -46,6 +46,7 @@ struct DgemmOptions {
   const double *cin = nullptr;
   int64_t ldci = 0;
   const int *gate = nullptr;
+  int gate_run_if_nonzero = 0;  // invert the gate: run only when *gate != 0
 };
 int dgemm_device_ex(int trans_a, int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B,
                     int64_t ldb, double *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st,
