@@ -54,6 +54,24 @@ int main(int argc, char **argv) {
     for (int q = 0; q < 4; ++q) ph[q] += ((q < 3 ? t[g * 4 + q + 1] : t[(g + 1) * 4]) - t[g * 4 + q]) / 1e3;
     ++cnt;
   }
+  {
+    std::vector<unsigned long long> ct(148 * 16 * 4);
+    cudaMemcpyFromSymbol(ct.data(), jac_cta_trace, ct.size() * 8);
+    int C = 0;
+    for (int b = 0; b < 148; ++b) if (ct[(b * 16) * 4]) C = b + 1;
+    for (int rr = 0; rr < 6; ++rr) {
+      unsigned long long s0 = ~0ull, s1 = 0, d0 = ~0ull, d1 = 0, e0 = ~0ull, e1 = 0;
+      for (int b = 0; b < C; ++b) {
+        auto *x = &ct[(b * 16 + rr) * 4];
+        s0 = std::min(s0, x[0]); s1 = std::max(s1, x[0]);
+        d0 = std::min(d0, x[1]); d1 = std::max(d1, x[1]);
+        e0 = std::min(e0, x[2]); e1 = std::max(e1, x[2]);
+      }
+      printf("round %d over %d CTAs: start spread %.2f us, steps-done spread %.2f, sends-done spread %.2f; "
+             "first start -> last steps done %.2f us\n", 100 + rr, C, (s1 - s0) / 1e3, (d1 - d0) / 1e3,
+             (e1 - e0) / 1e3, (d1 - s0) / 1e3);
+    }
+  }
   printf("rounds %d: phase us (grid kernel: steps/send/recv/-; gram kernel: gram/steps/apply/exchange): "
          "%.2f %.2f %.2f %.2f\n", cnt, ph[0] / cnt, ph[1] / cnt, ph[2] / cnt, ph[3] / cnt);
 }
