@@ -212,6 +212,58 @@ __global__ void __launch_bounds__(kThreads, 1)
       s_t = __dmul_rn(rs, epi.col_scale ? epi.col_scale[0] : 1.0);
       y_t = __drcp_rn(s_t);
     }
+    if constexpr (!TRANS && (EK == EK_F32 || EK == EK_F64)) {
+      // direct stores: thread = output row, 16 consecutive columns per TMEM load (64 B of fp32 /
+      // 128 B of fp64 per thread per chunk: whole sectors), no shared-memory staging or barriers
+      const bool vec = ((reinterpret_cast<uintptr_t>(epi.out) & 15) == 0) && (epi.ldo % 4 == 0);
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        const int cb = c0 + half * 16;
+        if (cb >= BN) continue;
+        uint32_t r[16];
+        if (nkb > 0) {
+          sm100::tmem_ld16(tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb, r);
+          sm100::tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) r[j] = 0;
+        }
+        if (row >= M) continue;
+        const int64_t col0 = n0 + cb;
+        double v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (tensor_scale) {
+            v[j] = div_exact((double)(int32_t)r[j], s_t, y_t);
+          } else {
+            const int64_t col = min(col0 + j, N - 1);
+            const double sc = __dmul_rn(rs, epi.col_scale[col * epi.col_scale_inc]);
+            v[j] = div_exact((double)(int32_t)r[j], sc, __drcp_rn(sc));
+          }
+          if constexpr (AB) v[j] = epi_alpha_beta(epi, v[j], row, min(col0 + j, N - 1));
+        }
+        const int64_t base = row * epi.ldo + col0;
+        if (vec && col0 + 16 <= N) {
+          if constexpr (EK == EK_F32) {
+            float4 *o = reinterpret_cast<float4 *>((float *)epi.out + base);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              o[q] = make_float4(__double2float_rn(v[4 * q]), __double2float_rn(v[4 * q + 1]),
+                                 __double2float_rn(v[4 * q + 2]), __double2float_rn(v[4 * q + 3]));
+          } else {
+            double2 *o = reinterpret_cast<double2 *>((double *)epi.out + base);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] = make_double2(v[2 * q], v[2 * q + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (col0 + j < N) {
+              if constexpr (EK == EK_F32) ((float *)epi.out)[base + j] = __double2float_rn(v[j]);
+              else ((double *)epi.out)[base + j] = v[j];
+            }
+        }
+      }
+    } else {
     double *tile = reinterpret_cast<double *>(smem);  // 128 x 33
     int32_t *itile = reinterpret_cast<int32_t *>(smem);
     for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -286,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
     }
   }
   sm100::tc_fence_before();
@@ -419,7 +472,8 @@ int igemm_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, 
   split_k = (int)ceil_div(kb_total, kb_per);
   const int BN = pick_bn(N);
   const int stage_bytes = BM * BK + BN * BK;
-  const int stages = std::max(2, std::min(8, (kSmemBudget - 2048) / stage_bytes));
+  // no more stages than k-blocks: short-K products (E2, E3) then fit two CTAs per SM
+  const int stages = std::max(2, std::min(std::min(8, kb_total), (kSmemBudget - 2048) / stage_bytes));
   const int smem = stages * stage_bytes + (2 * stages + 2) * 8 + 1024 + 64;
   CUtensorMap ta, tb;
   LRAMM_TRY(make_tmap_i8(&ta, a, M, K, lda, BM));
