@@ -4,8 +4,9 @@ Drop-in for the hot path of the reference package `lramm`
 (`pkg/src/lramm/__init__.py:6-76`): the same names for the pipeline, the
 randomised SVD, the quantiser and quantised GEMM, the parameter/timing
 dataclasses and the error types, computed by hand-written sm_100a CUDA
-(liblramm_cuda.so, C ABI in include/lramm_cuda.h).  Out of scope:
-bound evaluators, CLI, file I/O, input generators, evaluate/report.
+(liblramm_cuda.so, C ABI in include/lramm_cuda.h), plus the report path
+(`evaluate`, the closed-form bounds, `quantized_svd_approx`).  Out of scope (see
+DESIGN.md): CLI, file I/O, input generators.
 """
 
 from . import _native  # noqa: F401  (fails loudly if liblramm_cuda.so is missing)
@@ -37,6 +38,25 @@ from .quant import (
     integer_matmul,
     qgemm,
     quantize,
+)
+from .report import (
+    BoundInputs,
+    ErrorReport,
+    combined_bound,
+    evaluate,
+    frobenius_norm,
+    leading_sigmas,
+    lramm_general_bound,
+    lramm_specific_bound,
+    qgemm_bound,
+    qsvd_bound,
+    quant_matrix_bound,
+    quant_scalar_var_bound,
+    quantized_svd_approx,
+    relative_error,
+    rsvd_error_bound,
+    spectrum_shape_factor,
+    svd_trunc_bound,
 )
 from .rsvd import (
     RsvdParams,
