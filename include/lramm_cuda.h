@@ -197,6 +197,15 @@ int lramm_svd(const double *a, int64_t m, int64_t n, double *u, double *s, doubl
               void *ws, size_t ws_bytes, lramm_stream_t stream);
 size_t lramm_svd_ws(int64_t m, int64_t n);
 
+/* Gaussian test matrix on the device, bit-identical to NumPy's
+ * Generator(Philox(SeedSequence([seed, 0x534B, ncols, w]))).standard_normal((ncols, w))
+ * (matcore.py:89-92, rsvd.py:56): key0/key1 = the Philox key that SeedSequence produces
+ * (Philox(ss).state["state"]["key"]), out = ncols x w row-major fp64 on the device.
+ * Synchronous (a few tail draws are finished on the host with libm log1p). */
+int lramm_omega(uint64_t key0, uint64_t key1, int64_t ncols, int64_t w, double *out, void *ws, size_t ws_bytes,
+                lramm_stream_t stream);
+size_t lramm_omega_ws(int64_t ncols, int64_t w);
+
 /* Randomised SVD of x (rows x cols, F32 or F64) truncated to params->rank
  * (rsvd.py:68-94): u rows x rank, s rank, v cols x rank.  omega: cols x w fp64,
  * w = min(rank + oversample, min(rows, cols)), drawn by the caller exactly as

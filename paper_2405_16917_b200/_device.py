@@ -78,46 +78,54 @@ def to_device_matrix(a, device: torch.device, keep_f32: bool = True) -> torch.Te
 
 
 class OmegaCache:
-    """Gaussian test matrices drawn exactly as the reference (rsvd.py:56, matcore.py:89-92),
-    cached per (seed, ncols, width) on the host and per device."""
+    """Gaussian test matrices exactly as the reference draws them (rsvd.py:56, matcore.py:89-92):
+    generated on the device by lramm_omega (bit-identical to NumPy's Philox + standard_normal,
+    tests/test_gpu_omega.py), cached per (seed, ncols, width) on the device and, for the host
+    C-ABI path, as a page-locked host copy."""
 
     def __init__(self, capacity: int = 16):
         self.capacity = capacity
         self.host: OrderedDict = OrderedDict()
         self.dev: OrderedDict = OrderedDict()
-        self._pins: dict = {}
 
-    def host_omega(self, seed: int, ncols: int, width: int) -> np.ndarray:
-        key = (int(seed), int(ncols), int(width))
-        om = self.host.get(key)
-        if om is None:
-            entropy = [int(seed) & 0xFFFFFFFFFFFFFFFF, 0x534B, int(ncols), int(width)]
-            g = np.random.Generator(np.random.Philox(np.random.SeedSequence(entropy)))
-            om = np.ascontiguousarray(g.standard_normal((ncols, width)))
-            if torch.cuda.is_available():  # page-locked: the host API's upload is an async DMA
-                pinned = torch.empty(om.shape, dtype=torch.float64, pin_memory=True)
-                pinned.numpy()[...] = om
-                om = pinned.numpy()
-                self._pins[key] = pinned
-            self.host[key] = om
-            if len(self.host) > self.capacity:
-                old, _ = self.host.popitem(last=False)
-                self._pins.pop(old, None)
-        else:
-            self.host.move_to_end(key)
-        return om
+    @staticmethod
+    def philox_key(seed: int, ncols: int, width: int):
+        entropy = [int(seed) & 0xFFFFFFFFFFFFFFFF, 0x534B, int(ncols), int(width)]
+        key = np.random.Philox(np.random.SeedSequence(entropy)).state["state"]["key"]
+        return int(key[0]), int(key[1])
+
+    def _put(self, table, key, value):
+        table[key] = value
+        if len(table) > self.capacity:
+            table.popitem(last=False)
 
     def device_omega(self, seed: int, ncols: int, width: int, device: torch.device) -> torch.Tensor:
         key = (int(seed), int(ncols), int(width), device.index)
         t = self.dev.get(key)
         if t is None:
-            t = torch.from_numpy(self.host_omega(seed, ncols, width)).to(device)
-            self.dev[key] = t
-            if len(self.dev) > self.capacity:
-                self.dev.popitem(last=False)
+            from . import _native as N
+
+            t = torch.empty((ncols, width), dtype=torch.float64, device=device)
+            wsz = N.LIB.lramm_omega_ws(ncols, width)
+            ws = WORKSPACE.get(wsz, device)
+            k0, k1 = self.philox_key(seed, ncols, width)
+            N.check(N.LIB.lramm_omega(k0, k1, ncols, width, ptr(t), ptr(ws), wsz, stream_handle(device)))
+            self._put(self.dev, key, t)
         else:
             self.dev.move_to_end(key)
         return t
+
+    def host_omega(self, seed: int, ncols: int, width: int) -> np.ndarray:
+        key = (int(seed), int(ncols), int(width))
+        pinned = self.host.get(key)
+        if pinned is None:
+            dev = require_device()
+            pinned = torch.empty((ncols, width), dtype=torch.float64, pin_memory=True)
+            pinned.copy_(self.device_omega(seed, ncols, width, dev))
+            self._put(self.host, key, pinned)
+        else:
+            self.host.move_to_end(key)
+        return pinned.numpy()
 
 
 OMEGA = OmegaCache()

@@ -68,6 +68,9 @@ size_t rsvd_ws_bytes(int64_t, int64_t, const lramm_params_t &, int);
 int rsvd_device(const void *, int, int64_t, int64_t, const lramm_params_t &, const double *, double *, double *,
                 double *, int *, void *, size_t, cudaStream_t);
 size_t lramm_ws_bytes(int64_t, int64_t, int64_t, const lramm_params_t &, int);
+int omega_device(uint64_t key0, uint64_t key1, int64_t n, int64_t w, double *out, void *ws, size_t ws_bytes,
+                 cudaStream_t st);
+size_t omega_ws_bytes(int64_t n, int64_t w);
 int igemm_limbs_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, int64_t pa, int la,
                        const int8_t *b, int64_t ldb, int64_t pb, int lb, int64_t *acc64,
                        const lramm_epilogue_t &epi, cudaStream_t st);
@@ -182,6 +185,12 @@ int lramm_igemm(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, c
   if (!epi) return fail(LRAMM_ERR_PARAM, "igemm: epilogue is NULL");
   return igemm_device(M, N, K, a, lda, b, ldb, *epi, split_k, (cudaStream_t)stream);
 }
+
+int lramm_omega(uint64_t key0, uint64_t key1, int64_t ncols, int64_t w, double *out, void *ws, size_t ws_bytes,
+                lramm_stream_t stream) {
+  return omega_device(key0, key1, ncols, w, out, ws, ws_bytes, (cudaStream_t)stream);
+}
+size_t lramm_omega_ws(int64_t ncols, int64_t w) { return omega_ws_bytes(ncols, w); }
 
 int lramm_split_limbs(const int32_t *src, int64_t rows, int64_t cols, int64_t lds, int nlimb, int8_t *dst,
                       int64_t ldd, lramm_stream_t stream) {

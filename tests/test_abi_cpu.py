@@ -113,10 +113,52 @@ def test_child_seeds_match_oracle():
         assert _child_seeds(s) == O.child_seeds(s)
 
 
-def test_omega_matches_reference_generator():
-    import lramm_oracle as O
+def test_omega_key_and_ziggurat_tables_reproduce_numpy():
+    """The device Omega generator's inputs: the Philox key from SeedSequence, and the ziggurat
+    tables in csrc/ziggurat_tables.h, replayed by a scalar model of the draw against NumPy."""
+    import math
+    import os
+    import re
 
-    from paper_2405_16917_b200._device import OMEGA
+    import lramm_oracle as O  # noqa: F401
 
-    om = OMEGA.host_omega(77, 40, 9)
-    assert np.array_equal(om, O.gaussian_sketch(77, 40, 9))
+    from paper_2405_16917_b200._device import OmegaCache
+
+    k0, k1 = OmegaCache.philox_key(77, 40, 9)
+    st = np.random.Philox(np.random.SeedSequence([77, 0x534B, 40, 9])).state["state"]
+    assert (k0, k1) == (int(st["key"][0]), int(st["key"][1])) and not st["counter"].any()
+    hdr = open(os.path.join(os.path.dirname(__file__), "..", "paper_2405_16917_b200", "csrc",
+                            "ziggurat_tables.h")).read()
+
+    def table(name):
+        body = re.search(name + r"\[256\] = \{(.*?)\};", hdr, re.S).group(1)
+        return [float(v) if "." in v or "e" in v else int(v.replace("ULL", "")) for v in
+                [t.strip() for t in body.split(",") if t.strip()]]
+
+    K, W, F = table("kZigKHost"), table("kZigWHost"), table("kZigFHost")
+    R = float(re.search(r"kZigR = ([0-9.e+-]+);", hdr).group(1))
+    raw = np.random.Philox(np.random.SeedSequence([77, 0x534B, 40, 9])).random_raw(60000)
+    u = lambda v: (int(v) >> 11) * (1.0 / 9007199254740992.0)  # noqa: E731
+    out, i = [], 0
+    while len(out) < 40000:
+        r = int(raw[i]); i += 1
+        idx, r = r & 0xFF, r >> 8
+        sign, rabs = r & 1, (r >> 1) & 0x000FFFFFFFFFFFFF
+        x = -rabs * W[idx] if sign else rabs * W[idx]
+        if rabs < K[idx]:
+            out.append(x)
+        elif idx == 0:
+            while True:
+                xx, yy = -(1.0 / R) * math.log1p(-u(raw[i])), -math.log1p(-u(raw[i + 1]))
+                i += 2
+                if yy + yy > xx * xx:
+                    out.append(-(R + xx) if (rabs >> 8) & 1 else R + xx)
+                    break
+        elif (F[idx - 1] - F[idx]) * u(raw[i]) + F[idx] < math.exp(-0.5 * x * x):
+            i += 1
+            out.append(x)
+        else:
+            i += 1
+    ref = np.random.Generator(np.random.Philox(np.random.SeedSequence([77, 0x534B, 40, 9]))).standard_normal(40000)
+    assert np.array_equal(np.array(out), ref)
+    assert np.array_equal(O.gaussian_sketch(77, 40, 9).ravel(), ref[:360])  # the oracle's Omega is this stream
