@@ -392,11 +392,13 @@ def run_ours(args, cfg, world, rank, local):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
     wa = min(cfg["rank"] + cfg["oversample"], cfg["k"])
-    h2d = P * (4 * (cfg["m"] * cfg["k"] + cfg["k"] * cfg["n"]) + 8 * (cfg["k"] * wa + cfg["n"] * wa))
+    # A and B cross PCIe every step; Omega is generated on the device from the seed (lramm_omega)
+    h2d = P * 4 * (cfg["m"] * cfg["k"] + cfg["k"] * cfg["n"])
     d2h = P * 8 * cfg["m"] * cfg["n"]
     e2e = {"value": effective_ops(cfg) * P * world / e2e_s / 1e12, "unit": "TOPS", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
-           "path": "lramm(numpy) -> lramm_host_lramm (C ABI), pinned A/B/D, fp64 D like the reference"
+           "path": "lramm(numpy) -> lramm_host_lramm (C ABI), pinned A/B/D, fp64 D like the reference; "
+                   "Omega from the device generator (cached per seed)"
                    + ("; pairs issued one after another" if P > 1 else "")}
 
     # ---- dominant kernel + launches (live, torch profiler over device-resident steps)

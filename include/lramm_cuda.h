@@ -235,6 +235,8 @@ int lramm_host_imatmul(const int32_t *a, const int32_t *b, int64_t *out, int64_t
 int lramm_host_scale_round_clip(const double *a, int64_t m, int64_t n, double scale, int cap,
                                 int32_t *out);
 int lramm_host_svd(const double *a, int64_t m, int64_t n, double *u, double *s, double *v);
+/* a, b, c, d: host buffers (page-locked for asynchronous copies).  omega_a / omega_b: host
+ * buffers, or device buffers on the current device (e.g. from lramm_omega), used in place. */
 int lramm_host_lramm(const void *a, const void *b, int in_dtype, int64_t m, int64_t k, int64_t n,
                      const lramm_params_t *params, const double *omega_a, const double *omega_b,
                      const void *c, int c_dtype, void *d, int d_dtype, lramm_timings_t *timings);

@@ -423,17 +423,33 @@ int lramm_host_lramm(const void *a, const void *b, int in_dtype, int64_t m, int6
   // uploads overlap the factorisation: A and Omega_A on the compute stream (A's chain starts as
   // soon as they land), then B, Omega_B (and C) on the copy stream behind them; B's chain
   // waits only for its own operands (b_ready)
-  LRAMM_CUDA_TRY(cudaMemcpyAsync(oa, omega_a, k * wa * 8, cudaMemcpyHostToDevice, c.st));
+  // Omega may already live on this device (the device generator's cache): used in place
+  auto on_device = [&](const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeDevice && at.device == c.dev;
+  };
+  const double *oa_use = oa, *ob_use = ob;
+  if (on_device(omega_a))
+    oa_use = omega_a;
+  else
+    LRAMM_CUDA_TRY(cudaMemcpyAsync(oa, omega_a, k * wa * 8, cudaMemcpyHostToDevice, c.st));
   LRAMM_CUDA_TRY(cudaMemcpyAsync(da, a, m * k * es, cudaMemcpyHostToDevice, c.st));
   LRAMM_CUDA_TRY(cudaEventRecord(c.ev_a, c.st));
   LRAMM_CUDA_TRY(cudaStreamWaitEvent(c.copy, c.ev_a, 0));
-  LRAMM_CUDA_TRY(cudaMemcpyAsync(ob, omega_b, n * wb * 8, cudaMemcpyHostToDevice, c.copy));
+  if (on_device(omega_b))
+    ob_use = omega_b;
+  else
+    LRAMM_CUDA_TRY(cudaMemcpyAsync(ob, omega_b, n * wb * 8, cudaMemcpyHostToDevice, c.copy));
   LRAMM_CUDA_TRY(cudaMemcpyAsync(db, b, k * n * es, cudaMemcpyHostToDevice, c.copy));
   if (cmat) LRAMM_CUDA_TRY(cudaMemcpyAsync(dc, cmat, m * n * cs, cudaMemcpyHostToDevice, c.copy));
   LRAMM_CUDA_TRY(cudaEventRecord(c.ev_b, c.copy));
   if (timings) LRAMM_CUDA_TRY(cudaStreamWaitEvent(c.st, c.ev_b, 0));  // stage timings stay comparable
-  LRAMM_TRY(lramm_device(da, db, in_dtype, m, k, n, *params, oa, ob, dc, c_dtype, dd, d_dtype, c.status, w, ws,
-                         timings, c.st, c.ev_b));
+  LRAMM_TRY(lramm_device(da, db, in_dtype, m, k, n, *params, oa_use, ob_use, dc, c_dtype, dd, d_dtype, c.status, w,
+                         ws, timings, c.st, c.ev_b));
   LRAMM_CUDA_TRY(cudaMemcpyAsync(d, dd, m * n * ds, cudaMemcpyDeviceToHost, c.st));
   return finish(c);
 }

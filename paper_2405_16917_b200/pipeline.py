@@ -251,8 +251,9 @@ def lramm(a, b, params, c=None, out=None):
     seed_a, seed_b = _child_seeds(params.seed)
     wa = sketch_width((m, k), params.rank, params.oversample)
     wb = sketch_width((k, n), params.rank, params.oversample)
-    om_a = OMEGA.host_omega(seed_a, k, wa)
-    om_b = OMEGA.host_omega(seed_b, n, wb)
+    dev = require_device()
+    om_a = OMEGA.device_omega(seed_a, k, wa, dev)  # device-resident: the C ABI uses them in place
+    om_b = OMEGA.device_omega(seed_b, n, wb, dev)
     out_dt = np.dtype(params.out_dtype)
     if out is not None:
         if out.shape != (m, n) or out.dtype != out_dt or not out.flags["C_CONTIGUOUS"]:
@@ -264,7 +265,8 @@ def lramm(a, b, params, c=None, out=None):
     t = N.Timings()
     vp = lambda x: ctypes.c_void_p(x.ctypes.data) if x is not None else ctypes.c_void_p(0)  # noqa: E731
     rc = N.LIB.lramm_host_lramm(vp(ha), vp(hb), N.F32 if in_dt == np.float32 else N.F64, m, k, n, ctypes.byref(p),
-                                vp(om_a), vp(om_b), vp(hc), N.F64, vp(d), N.F32 if out_dt == np.float32 else N.F64,
+                                ctypes.c_void_p(om_a.data_ptr()), ctypes.c_void_p(om_b.data_ptr()), vp(hc), N.F64, vp(d),
+                                N.F32 if out_dt == np.float32 else N.F64,
                                 ctypes.byref(t))
     N.check(rc)
     return d, _timings_from(t, m, n, k, params)
