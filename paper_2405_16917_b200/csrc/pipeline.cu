@@ -101,6 +101,7 @@ struct RsvdBufs {
   int32_t *acc = nullptr;
   int *info = nullptr, *compl_st = nullptr, *nonfinite = nullptr;
   void *qr_ws = nullptr, *svd_ws = nullptr, *gemm_ws = nullptr, *qz_ws = nullptr;
+  void *qz_ws2 = nullptr;  // quantiser scratch of the helper stream (operand copies made off the critical path)
   size_t qr_bytes = 0, svd_bytes = 0, gemm_bytes = 0, qz_bytes = 0;
 };
 
@@ -136,6 +137,7 @@ RsvdBufs carve_rsvd(Arena &ar, int64_t rows, int64_t cols, int x_dtype, const lr
     b.qzq = take_qop(ar, w, cols, row ? w : 1);
     b.qz_bytes = quantize_ws_bytes(std::max(rows, cols), std::max(rows, cols));
     b.qz_ws = ar.take<char>((int64_t)b.qz_bytes);
+    b.qz_ws2 = ar.take<char>((int64_t)b.qz_bytes);
     int64_t mx = std::max(rows, cols);
     b.acc = ar.take<int32_t>(mx * w);
   } else if (x_dtype == LRAMM_F32) {
@@ -234,6 +236,28 @@ int check_acc(int64_t K, int bits_a, int bits_b) {
   return LRAMM_OK;
 }
 
+// helper stream per (device, chain stream): the quantised copies of X that the power iteration
+// and the projection need (X row-scaled at power_bits, X^T column-scaled) depend only on X, so
+// they are made while the sketch's QR runs
+struct HelperStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+HelperStream &helper_stream(cudaStream_t main) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, HelperStream> table;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  HelperStream &x = table[{dev, main}];
+  if (!x.st) {
+    cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+  }
+  return x;
+}
+
 int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, const double *omega, double *U,
              int64_t ldu, double *S, double *V, int64_t ldv, cudaStream_t st) {
   const int64_t rows = b.rows, cols = b.cols, w = b.w, r = b.r;
@@ -243,6 +267,36 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
   const int gran_l = b.gran == LRAMM_GRAN_ROW ? LRAMM_GRAN_ROW : LRAMM_GRAN_TENSOR;  // left operand rows
   const int gran_r = b.gran == LRAMM_GRAN_ROW ? LRAMM_GRAN_COL : LRAMM_GRAN_TENSOR;  // right operand columns
   const double *x64 = (const double *)x;
+  bool helper = false;
+  HelperStream *hs = nullptr;
+  const bool need_xp_row = b.fast && P.power_iters > 0 && b.xr_p.q != b.xr_s.q;
+  const bool need_xc_p = b.fast && P.power_iters > 0;
+  const bool need_xc_j = b.fast && (b.xc_j.q != b.xc_p.q || P.power_iters == 0);
+  if (b.fast) {
+    // the X-only operand copies on the helper stream (joined before their first use)
+    hs = &helper_stream(st);
+    LRAMM_CUDA_TRY(cudaEventRecord(hs->fork, st));
+    LRAMM_CUDA_TRY(cudaStreamWaitEvent(hs->st, hs->fork, 0));
+    const int gran_c = gran_r == LRAMM_GRAN_COL ? LRAMM_GRAN_COL : LRAMM_GRAN_TENSOR;
+    if (need_xp_row)
+      LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.power_bits, gran_l, 0, b.xr_p, b.nonfinite, b.qz_ws2, b.qz_bytes,
+                      hs->st));
+    if (need_xc_p)
+      LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.power_bits, gran_c, 1, b.xc_p, b.nonfinite, b.qz_ws2, b.qz_bytes,
+                      hs->st));
+    if (need_xc_j)
+      LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.proj_bits, gran_c, 1, b.xc_j, b.nonfinite, b.qz_ws2, b.qz_bytes,
+                      hs->st));
+    LRAMM_CUDA_TRY(cudaEventRecord(hs->join, hs->st));
+    helper = true;
+  }
+  auto join_helper = [&]() -> int {
+    if (helper) {
+      LRAMM_CUDA_TRY(cudaStreamWaitEvent(st, hs->join, 0));
+      helper = false;
+    }
+    return LRAMM_OK;
+  };
   if (b.fast) {
     // Y = X . Omega at sketch_bits
     LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.sketch_bits, gran_l, 0, b.xr_s, b.nonfinite, b.qz_ws, b.qz_bytes, st));
@@ -257,12 +311,7 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
     LRAMM_TRY(dgemm_device(0, rows, w, cols, x64, cols, omega, w, b.Y, w, b.gemm_ws, b.gemm_bytes, st));
   }
   LRAMM_TRY(qr_device(b.Y, rows, w, w, b.Q, w, nullptr, b.qr_ws, b.qr_bytes, st));
-  if (b.fast && P.power_iters > 0) {
-    if (b.xr_p.q != b.xr_s.q)
-      LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.power_bits, gran_l, 0, b.xr_p, b.nonfinite, b.qz_ws, b.qz_bytes, st));
-    LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.power_bits, gran_r == LRAMM_GRAN_COL ? LRAMM_GRAN_COL : LRAMM_GRAN_TENSOR,
-                    1, b.xc_p, b.nonfinite, b.qz_ws, b.qz_bytes, st));
-  }
+  if (b.fast && P.power_iters > 0) LRAMM_TRY(join_helper());
   for (int it = 0; it < P.power_iters; ++it) {
     // Z = X^T Q ; Qz = qr(Z) ; Y = X Qz ; Q = qr(Y)   (rsvd.py:60-64)
     if (b.fast) {
@@ -282,9 +331,7 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
   }
   // Bs^T = X^T Q   (rsvd.py:77, evaluated transposed)
   if (b.fast) {
-    if (b.xc_j.q != b.xc_p.q || P.power_iters == 0)
-      LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.proj_bits, gran_r == LRAMM_GRAN_COL ? LRAMM_GRAN_COL : LRAMM_GRAN_TENSOR,
-                      1, b.xc_j, b.nonfinite, b.qz_ws, b.qz_bytes, st));
+    LRAMM_TRY(join_helper());
     LRAMM_TRY(quant(b.Q, LRAMM_F64, rows, w, w, P.proj_bits, gran_r, 1, b.qq, nullptr, b.qz_ws, b.qz_bytes, st));
     LRAMM_TRY(qprod(b.xc_j, b.qq, cols, w, rows, b.BsT, w, 0, b.acc, st));
   } else {
