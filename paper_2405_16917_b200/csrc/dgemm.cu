@@ -226,7 +226,10 @@ int64_t tile_count(int64_t M, int64_t N, bool sym) {
 
 int choose_splits(int trans_a, int64_t M, int64_t N, int64_t K, bool sym = false) {
   int64_t tiles = tile_count(M, N, sym);
-  int64_t want = ceil_div(3LL * num_sms(), tiles);  // ~3 resident CTAs per SM
+  // ~4 waves of 4 resident CTAs per SM when K is long enough (wave quantisation stays small);
+  // each split keeps >= 256 of K (max_by_k)
+  if (tiles >= 4LL * num_sms()) return 1;  // already a full wave of tiles: no partials
+  int64_t want = ceil_div(16LL * num_sms(), tiles);
   int64_t max_by_k = std::max<int64_t>(1, K / 256);
   int64_t s = std::max<int64_t>(1, std::min<int64_t>(want, std::min<int64_t>(max_by_k, 64)));
   return (int)s;
