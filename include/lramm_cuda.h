@@ -127,6 +127,16 @@ int lramm_quantize(const void *x, int x_dtype, int64_t rows, int64_t cols, int64
                    lramm_stream_t stream);
 size_t lramm_quantize_ws(int64_t rows, int64_t cols);
 
+/* Two int8 quantisations of one x from one absmax pass and one read of x: q_r = x row-major at
+ * (bits_r, granularity_r) and q_t = x^T at (bits_t, granularity_t); granularities are in x's
+ * coordinates (ROW = per row of x, COL = per column of x).  Each is bit-identical to the matching
+ * lramm_quantize call (quant.py:55-71 applied twice to the same x); bits <= 8.
+ * ws >= lramm_quantize_ws(rows, cols). */
+int lramm_quantize_pair(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits_r,
+                        int granularity_r, int8_t *q_r, int64_t ldq_r, double *scales_r, int bits_t,
+                        int granularity_t, int8_t *q_t, int64_t ldq_t, double *scales_t, int *nonfinite_flag,
+                        void *ws, size_t ws_bytes, lramm_stream_t stream);
+
 /* max |x| per tensor / row / column (exact; amax must be zeroed by the caller: the kernel takes a
  * max into it, so partial results of several shards can be combined with an allreduce(MAX)). */
 int lramm_absmax(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int granularity, double *amax,

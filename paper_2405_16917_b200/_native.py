@@ -84,6 +84,8 @@ SIGNATURES = {
     "lramm_quantize_ws": (_sz, [_i64, _i64]),
     "lramm_scale_round_clip": (_i32, [_vp, _i64, _i64, _i64, _d, _i32, _vp, _i64, _vp]),
     "lramm_absmax": (_i32, [_vp, _i32, _i64, _i64, _i64, _i32, _vp, _vp, _vp]),
+    "lramm_quantize_pair": (_i32, [_vp, _i32, _i64, _i64, _i64, _i32, _i32, _vp, _i64, _vp, _i32, _i32, _vp, _i64, _vp,
+                                   _vp, _vp, _sz, _vp]),
     "lramm_quantize_amax": (_i32, [_vp, _i32, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _i32, _i64, _vp, _vp]),
     "lramm_cholqr_pass": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "lramm_cholqr_pass_ws": (_sz, [_i64, _i64]),

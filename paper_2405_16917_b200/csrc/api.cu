@@ -45,6 +45,8 @@ int num_sms() {
 int quantize_device(const void *, int, int64_t, int64_t, int64_t, int, int, int, void *, int, int64_t, double *, int *,
                     void *, size_t, cudaStream_t);
 size_t quantize_ws_bytes(int64_t, int64_t);
+int quantize_pair_device(const void *, int, int64_t, int64_t, int64_t, int, int, int8_t *, int64_t, double *, int, int,
+                         int8_t *, int64_t, double *, int *, void *, size_t, cudaStream_t);
 int absmax_device(const void *, int, int64_t, int64_t, int64_t, int, double *, int *, cudaStream_t);
 int quantize_amax_device(const void *, int, int64_t, int64_t, int64_t, int, int, int, const double *, void *, int, int64_t,
                          double *, cudaStream_t);
@@ -150,6 +152,14 @@ int lramm_quantize(const void *x, int x_dtype, int64_t rows, int64_t cols, int64
                          nonfinite_flag, ws, ws_bytes, (cudaStream_t)stream);
 }
 size_t lramm_quantize_ws(int64_t rows, int64_t cols) { return quantize_ws_bytes(rows, cols); }
+
+int lramm_quantize_pair(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits_r,
+                        int granularity_r, int8_t *q_r, int64_t ldq_r, double *scales_r, int bits_t,
+                        int granularity_t, int8_t *q_t, int64_t ldq_t, double *scales_t, int *nonfinite_flag,
+                        void *ws, size_t ws_bytes, lramm_stream_t stream) {
+  return quantize_pair_device(x, x_dtype, rows, cols, ldx, bits_r, granularity_r, q_r, ldq_r, scales_r, bits_t,
+                              granularity_t, q_t, ldq_t, scales_t, nonfinite_flag, ws, ws_bytes, (cudaStream_t)stream);
+}
 
 int lramm_absmax(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int granularity, double *amax,
                  int *nonfinite_flag, lramm_stream_t stream) {

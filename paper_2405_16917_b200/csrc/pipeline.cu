@@ -23,6 +23,9 @@ int quantize_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int6
                     int transpose, void *q, int q_dtype, int64_t ldq, double *scales, int *nonfinite, void *ws,
                     size_t ws_bytes, cudaStream_t st);
 size_t quantize_ws_bytes(int64_t rows, int64_t cols);
+int quantize_pair_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits_r, int gran_r,
+                         int8_t *qr, int64_t ldqr, double *scales_r, int bits_t, int gran_t, int8_t *qt, int64_t ldqt,
+                         double *scales_t, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st);
 int igemm_limbs_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, int64_t pa, int la,
                        const int8_t *b, int64_t ldb, int64_t pb, int lb, int64_t *acc64,
                        const lramm_epilogue_t &epi, cudaStream_t st);
@@ -269,15 +272,20 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
   const double *x64 = (const double *)x;
   bool helper = false;
   HelperStream *hs = nullptr;
+  const int gran_c = gran_r == LRAMM_GRAN_COL ? LRAMM_GRAN_COL : LRAMM_GRAN_TENSOR;  // X^T copies: per input column
+  // the first transposed copy X^T needs (power iteration, else projection) is written by the same
+  // pass that quantises X for the sketch: one absmax pass + one read of X for both layouts
+  QOp &xc_first = P.power_iters > 0 ? b.xc_p : b.xc_j;
+  const int bits_first = P.power_iters > 0 ? P.power_bits : P.proj_bits;
+  const bool pair = b.fast && b.xr_s.limbs <= 1 && xc_first.limbs <= 1;
   const bool need_xp_row = b.fast && P.power_iters > 0 && b.xr_p.q != b.xr_s.q;
-  const bool need_xc_p = b.fast && P.power_iters > 0;
-  const bool need_xc_j = b.fast && (b.xc_j.q != b.xc_p.q || P.power_iters == 0);
-  if (b.fast) {
-    // the X-only operand copies on the helper stream (joined before their first use)
+  const bool need_xc_p = b.fast && P.power_iters > 0 && !pair;
+  const bool need_xc_j = b.fast && (b.xc_j.q != b.xc_p.q || P.power_iters == 0) && !(pair && P.power_iters == 0);
+  if (need_xp_row || need_xc_p || need_xc_j) {
+    // the remaining X-only operand copies on the helper stream (joined before their first use)
     hs = &helper_stream(st);
     LRAMM_CUDA_TRY(cudaEventRecord(hs->fork, st));
     LRAMM_CUDA_TRY(cudaStreamWaitEvent(hs->st, hs->fork, 0));
-    const int gran_c = gran_r == LRAMM_GRAN_COL ? LRAMM_GRAN_COL : LRAMM_GRAN_TENSOR;
     if (need_xp_row)
       LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.power_bits, gran_l, 0, b.xr_p, b.nonfinite, b.qz_ws2, b.qz_bytes,
                       hs->st));
@@ -299,7 +307,13 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
   };
   if (b.fast) {
     // Y = X . Omega at sketch_bits
-    LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.sketch_bits, gran_l, 0, b.xr_s, b.nonfinite, b.qz_ws, b.qz_bytes, st));
+    if (pair)
+      LRAMM_TRY(quantize_pair_device(x, x_dtype, rows, cols, cols, P.sketch_bits, gran_l, b.xr_s.q, b.xr_s.ld,
+                                     b.xr_s.scale, bits_first, gran_c, xc_first.q, xc_first.ld, xc_first.scale,
+                                     b.nonfinite, b.qz_ws, b.qz_bytes, st));
+    else
+      LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.sketch_bits, gran_l, 0, b.xr_s, b.nonfinite, b.qz_ws, b.qz_bytes,
+                      st));
     LRAMM_TRY(quant(omega, LRAMM_F64, cols, w, w, P.sketch_bits, gran_r, 1, b.om, nullptr, b.qz_ws, b.qz_bytes, st));
     LRAMM_TRY(qprod(b.xr_s, b.om, rows, w, cols, b.Y, w, 0, b.acc, st));
   } else {

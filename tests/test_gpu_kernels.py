@@ -103,6 +103,69 @@ def test_quantize_granularity_layouts(N, gran, transpose, dtype):
     assert not pad.any()
 
 
+def _oracle_quant(x, bits, gran):
+    if gran == "tensor":
+        d, s = O.quantize_tensor(x, bits)
+        return d, np.array([s])
+    return (O.quantize_rows if gran == "row" else O.quantize_cols)(x, bits)
+
+
+@pytest.mark.parametrize("shape", [(77, 45), (130, 300), (1, 5), (300, 1), (64, 64)])
+@pytest.mark.parametrize("grans,bits", [(("tensor", "tensor"), (8, 8)), (("row", "col"), (8, 8)),
+                                        (("row", "col"), (4, 8)), (("col", "tensor"), (6, 3)),
+                                        (("row", "row"), (8, 8))])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("strided", [False, True])
+def test_quantize_pair_bit_exact(N, shape, grans, bits, dtype, strided):
+    """lramm_quantize_pair: both layouts equal two independent quantisations (quant.py:55-71)."""
+    rows, cols = shape
+    base = O.generate(rows, cols + (3 if strided else 0), "normal", rows + cols).astype(dtype)
+    base[0, : min(cols, 4)] = 0.0
+    x = base[:, :cols]
+    t = torch.from_numpy(base).to(dev())[:, :cols]  # ld = cols + 3: the unvectorised path
+    code = {"tensor": N.GRAN_TENSOR, "row": N.GRAN_ROW, "col": N.GRAN_COL}
+    ldr, ldt = ((cols + 15) // 16) * 16, ((rows + 15) // 16) * 16
+    qr = torch.full((rows, ldr), 99, dtype=torch.int8, device=dev())
+    qt = torch.full((cols, ldt), 99, dtype=torch.int8, device=dev())
+    ns = {"tensor": 1, "row": rows, "col": cols}
+    sr = torch.empty(ns[grans[0]], dtype=torch.float64, device=dev())
+    st = torch.empty(ns[grans[1]], dtype=torch.float64, device=dev())
+    flag = torch.zeros(1, dtype=torch.int32, device=dev())
+    wsz = N.LIB.lramm_quantize_ws(rows, cols)
+    ws = torch.empty(wsz, dtype=torch.uint8, device=dev())
+    vp = ctypes.c_void_p
+    N.check(N.LIB.lramm_quantize_pair(vp(t.data_ptr()), N.F32 if dtype == np.float32 else N.F64, rows, cols,
+                                      t.stride(0), bits[0], code[grans[0]], vp(qr.data_ptr()), ldr,
+                                      vp(sr.data_ptr()), bits[1], code[grans[1]], vp(qt.data_ptr()), ldt,
+                                      vp(st.data_ptr()), vp(flag.data_ptr()), vp(ws.data_ptr()), wsz,
+                                      vp(torch.cuda.current_stream().cuda_stream)))
+    dr, srf = _oracle_quant(x, bits[0], grans[0])
+    dt, stf = _oracle_quant(x, bits[1], grans[1])
+    got_r, got_t = qr.cpu().numpy(), qt.cpu().numpy()
+    assert np.array_equal(got_r[:, :cols].astype(np.int32), dr)
+    assert np.array_equal(got_t[:, :rows].T.astype(np.int32), dt)
+    assert np.array_equal(sr.cpu().numpy(), srf) and np.array_equal(st.cpu().numpy(), stf)
+    assert not got_r[:, cols:].any() and not got_t[:, rows:].any()
+    assert int(flag.item()) == 0
+
+
+def test_quantize_pair_nonfinite_flag(N):
+    x = torch.ones((40, 70), dtype=torch.float32, device=dev())
+    x[5, 9] = float("nan")
+    qr = torch.empty((40, 80), dtype=torch.int8, device=dev())
+    qt = torch.empty((70, 48), dtype=torch.int8, device=dev())
+    s = torch.empty(2, dtype=torch.float64, device=dev())
+    flag = torch.zeros(1, dtype=torch.int32, device=dev())
+    wsz = N.LIB.lramm_quantize_ws(40, 70)
+    ws = torch.empty(wsz, dtype=torch.uint8, device=dev())
+    vp = ctypes.c_void_p
+    N.check(N.LIB.lramm_quantize_pair(vp(x.data_ptr()), N.F32, 40, 70, 70, 8, N.GRAN_TENSOR, vp(qr.data_ptr()), 80,
+                                      vp(s.data_ptr()), 8, N.GRAN_TENSOR, vp(qt.data_ptr()), 48,
+                                      vp(s.data_ptr() + 8), vp(flag.data_ptr()), vp(ws.data_ptr()), wsz,
+                                      vp(torch.cuda.current_stream().cuda_stream)))
+    assert int(flag.item()) == 1
+
+
 # ------------------------------------------------------------------ integer GEMM
 
 
