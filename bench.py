@@ -410,6 +410,7 @@ def run_ours(args, cfg, world, rank, local):
     roof["us_per_launch"] = top_us
     roof["launches_per_step"] = top_per_step
     roof["share_of_step"] = top_us * top_per_step / step_us if step_us else None
+    stages = stage_rooflines(per, 5, cfg, peaks) if per else None
 
     line = {"metric": "effective approx-GEMM TOPS (2mnk/time)", "value": value, "unit": "TOPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -417,7 +418,8 @@ def run_ours(args, cfg, world, rank, local):
             "dtype": "int8 x int8 -> int32 (tcgen05) sketch/QM GEMMs; fp64 factorisation; fp32 D",
             "data": "synthetic (SURVEY §8(d) spectrum, Haar factors from seeded torch QR)",
             "config": workload_config(cfg, args, world), "clocks": clock_summary, "e2e": e2e,
-            "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches, "roofline": roof}
+            "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches, "roofline": roof,
+            "stages": stages}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in CPU_SAMPLE_CONFIGS:
         line["cpu_baseline"] = cpu_baseline(cfg, a, b)
     if rank == 0:
@@ -568,6 +570,58 @@ def dominant_roofline(name, us, cfg, peaks):
     achieved = byts / (us * 1e-6) / 1e9
     return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
             "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+
+
+STAGES = (  # kernel-name fragments -> stage of the hot path
+    ("omega", ("omega",)),
+    ("quantize", ("absmax", "quantize", "scales_from", "split_limbs")),
+    ("int8_gemm", ("igemm", "epilogue")),
+    ("jacobi_svd", ("jacobi", "col_norms", "rank_kernel", "finalize_write", "complete_kernel", "scale_cols")),
+    ("fp64_qr", ("dgemm", "chol", "trsm", "cf_prep", "splitk", "transpose", "householder", "diag_inv",
+                 "set_identity", "any_nonzero")),
+)
+
+
+def stage_rooflines(per, reps, cfg, peaks, sweeps=10):
+    """Per-stage device time (kernel time summed over both operand chains, per step) against the
+    stage's roofline time max(ops / peak, bytes / HBM) from its algorithmic work."""
+    m, k, n, r, q = cfg["m"], cfg["k"], cfg["n"], cfg["rank"], cfg["power_iters"]
+    w = min(r + cfg["oversample"], m, k, n)
+    hbm = peaks.get("hbm_gbs", 6538.0) * 1e9
+    fp64 = 36.7e12  # measured DFMA/DMMA peak (profiles/r01_fp64_peak.txt)
+    int8 = 4.5e15   # nominal dense int8 tcgen05 (no measured int8 figure in MEASURED_PEAKS.json)
+    # quantiser: fp32 operands read once, two int8 copies written; fp64 sketch/recombination operands 8 B + 1 B
+    q_bytes = 6 * (m * k + k * n) + 9 * ((k * w + q * (m * w + k * w) + m * w) + (n * w + q * (k * w + n * w) + k * w)
+                                         + (r * k + k * r) + (r * r + r * n) + (m * r + r * n))
+    prods = [(m, w, k, 8)] * (1 + q) + [(k, w, m, 8)] * (q + 1) + [(k, w, n, 8)] * (1 + q) + [(n, w, k, 8)] * (q + 1)
+    prods += [(r, r, k, 8), (r, n, r, 8), (m, n, r, 4)]
+    g_ops = sum(2.0 * M * N * K for M, N, K, _ in prods)
+    g_bytes = sum(M * K + N * K + M * N * ob for M, N, K, ob in prods)
+    qr_rows = [m] * (1 + q) + [k] * q + [k] + [k] * (1 + q) + [n] * q + [n]
+    qr_flops = sum(6.0 * rr * w * w for rr in qr_rows) + 2.0 * (m + k) * w * w + 2.0 * (k + n) * w * w
+    jac_flops = 2 * sweeps * (w * (w - 1) / 2) * 8 * w
+    work = {
+        "omega": (0.0, 8.0 * (k + n) * w, "bytes: Omega_A, Omega_B written (fp64)"),
+        "quantize": (0.0, float(q_bytes), "bytes: fp32 operands read once + 2 int8 copies; fp64 sketch and "
+                                         "recombination operands read + int8 written"),
+        "int8_gemm": (g_ops / int8, float(g_bytes), "2MNK over the sketch/projection/recombination products; "
+                                                   "int8 operands read + outputs written"),
+        "fp64_qr": (qr_flops / fp64, 0.0, "6 rows w^2 per CholeskyQR2 + the two lifts (fp64 tensor peak)"),
+        "jacobi_svd": (jac_flops / fp64, 0.0, f"{sweeps} sweeps x w(w-1)/2 pairs x 8w flops, two operands"),
+    }
+    out = {}
+    for stage, frags in STAGES:
+        us = sum(v[0] for name, v in per.items() if any(f in name for f in frags)) / reps
+        t_ops, byts, what = work[stage]
+        roof_us = max(t_ops, byts / hbm) * 1e6
+        out[stage] = {"us_per_step": us, "roofline_us": roof_us, "frac": (roof_us / us) if us else None,
+                      "bound": "hbm" if byts / hbm >= t_ops else ("int8 tensor" if stage == "int8_gemm" else "fp64"),
+                      "work": what}
+    known = sum(v["us_per_step"] for v in out.values())
+    out["other"] = {"us_per_step": sum(v[0] for v in per.values()) / reps - known}
+    out["note"] = ("kernel time summed over the concurrent A/B chains (torch profiler over device-resident steps, "
+                   "outside the timed region); frac = roofline time / measured time")
+    return out
 
 
 def cpu_baseline(cfg, a, b):

@@ -40,7 +40,7 @@ int dgemm_device(int trans_a, int64_t M, int64_t N, int64_t K, const double *A, 
                  int64_t ldb, double *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st);
 size_t dgemm_ws_bytes(int trans_a, int64_t M, int64_t N, int64_t K);
 int qr_device(const double *y, int64_t m, int64_t w, int64_t ldy, double *q, int64_t ldq, double *r, void *ws,
-              size_t ws_bytes, cudaStream_t st);
+              size_t ws_bytes, cudaStream_t st, bool q_needed = true);
 size_t qr_ws_bytes(int64_t m, int64_t w);
 int svd_tall_device(const double *T, int64_t m, int64_t n, int64_t ldt, double *pside, int64_t ldp, double *s,
                     double *h, int64_t ldh, int *info, int *status, void *ws, size_t ws_bytes, cudaStream_t st);

@@ -26,8 +26,25 @@ p = L.LrammParams(rank=cfg["rank"], bits=tuple(cfg["bits"]), power_iters=cfg["po
 for _ in range(3):
     L.lramm_device(a, b, p)
 torch.cuda.synchronize()
+use_graph = os.environ.get("TIMELINE_GRAPH", "1") == "1"
+if use_graph:  # the bench's execution mode: one step captured into a CUDA graph
+    cap = torch.cuda.Stream(device=dev)
+    cap.wait_stream(torch.cuda.current_stream(dev))
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(cap):
+        L.lramm_device(a, b, p)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=cap):
+            L.lramm_device(a, b, p)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    L.lramm_device(a, b, p)
+    if use_graph:
+        graph.replay()
+    else:
+        L.lramm_device(a, b, p)
     torch.cuda.synchronize()
 evs = []
 for ev in prof.events():
@@ -48,7 +65,6 @@ for sid, lst in streams.items():
     print(f"   idle between kernels {tot_gap:.0f} us; largest gaps:")
     for g, a_, b_, at in sorted(gaps, reverse=True)[:6]:
         print(f"     {g:7.1f} us at {at:7.0f}: after {a_} before {b_}")
-    # coarse phases
     for s, e, nm in lst:
-        if e - s > 80:
+        if e - s > float(os.environ.get("TIMELINE_MIN_US", "80")):
             print(f"   {s:8.0f} .. {e:8.0f}  {e - s:7.0f} us  {nm}")
