@@ -5,13 +5,15 @@ Drop-in for the hot path of the reference package `lramm`
 randomised SVD, the quantiser and quantised GEMM, the parameter/timing
 dataclasses and the error types, computed by hand-written sm_100a CUDA
 (liblramm_cuda.so, C ABI in include/lramm_cuda.h), plus the report path
-(`evaluate`, the closed-form bounds, `quantized_svd_approx`).  Out of scope (see
-DESIGN.md): CLI, file I/O, input generators.
+(`evaluate`, the closed-form bounds, `quantized_svd_approx`), and the CLI front end
+(`cli.py`: gen / mm / sweep / spectrum / profile, LRMM and CSV files and the seeded
+generators on the host in `matio.py`).
 """
 
 from . import _native  # noqa: F401  (fails loudly if liblramm_cuda.so is missing)
 from .errors import (
     DegenerateDenominatorError,
+    FormatError,
     LrammError,
     OracleLimitError,
     OverflowRiskError,
