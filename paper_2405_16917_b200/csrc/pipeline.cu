@@ -42,6 +42,9 @@ size_t dgemm_ws_bytes(int trans_a, int64_t M, int64_t N, int64_t K);
 int qr_device(const double *y, int64_t m, int64_t w, int64_t ldy, double *q, int64_t ldq, double *r, void *ws,
               size_t ws_bytes, cudaStream_t st, bool q_needed = true);
 size_t qr_ws_bytes(int64_t m, int64_t w);
+int svd_tall_pside_device(const double *T, int64_t m, int64_t n, int64_t ldt, const double *s, const double *H,
+                          int64_t ldh, double *pside, int64_t ldp, int *status, void *ws, size_t ws_bytes,
+                          cudaStream_t st);
 int svd_tall_device(const double *T, int64_t m, int64_t n, int64_t ldt, double *pside, int64_t ldp, double *s,
                     double *h, int64_t ldh, int *info, int *status, void *ws, size_t ws_bytes, cudaStream_t st);
 size_t svd_tall_ws_bytes(int64_t m, int64_t n);
@@ -352,12 +355,21 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
     LRAMM_TRY(dgemm_device(1, cols, w, rows, x64, cols, b.Q, w, b.BsT, w, b.gemm_ws, b.gemm_bytes, st));
   }
   // SVD(Bs): u = H, v = Bs^T H diag(s)^-1   (rsvd.py:78, _jacobi.py)
-  LRAMM_TRY(svd_tall_device(b.BsT, cols, w, w, b.Pside, w, b.s, b.H, w, b.info, b.compl_st, b.svd_ws, b.svd_bytes, st));
-  // lift U = Q u (rsvd.py:79) and truncate (rsvd.py:84-94)
+  LRAMM_TRY(svd_tall_device(b.BsT, cols, w, w, nullptr, w, b.s, b.H, w, b.info, b.compl_st, b.svd_ws, b.svd_bytes,
+                             st));
+  // v = Bs^T H diag(s)^-1 on the helper stream, concurrent with the lift U = Q u (rsvd.py:79-81);
+  // both then truncated to r (rsvd.py:84-94)
+  HelperStream &hv = helper_stream(st);
+  LRAMM_CUDA_TRY(cudaEventRecord(hv.fork, st));
+  LRAMM_CUDA_TRY(cudaStreamWaitEvent(hv.st, hv.fork, 0));
+  LRAMM_TRY(svd_tall_pside_device(b.BsT, cols, w, w, b.s, b.H, w, b.Pside, w, b.compl_st, b.svd_ws, b.svd_bytes,
+                                  hv.st));
+  LRAMM_CUDA_TRY(cudaMemcpy2DAsync(V, ldv * sizeof(double), b.Pside, w * sizeof(double), r * sizeof(double), cols,
+                                   cudaMemcpyDeviceToDevice, hv.st));
+  LRAMM_CUDA_TRY(cudaEventRecord(hv.join, hv.st));
   LRAMM_TRY(dgemm_device(0, rows, r, w, b.Q, w, b.H, w, U, ldu, b.gemm_ws, b.gemm_bytes, st));
   LRAMM_CUDA_TRY(cudaMemcpyAsync(S, b.s, r * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  LRAMM_CUDA_TRY(cudaMemcpy2DAsync(V, ldv * sizeof(double), b.Pside, w * sizeof(double), r * sizeof(double), cols,
-                                   cudaMemcpyDeviceToDevice, st));
+  LRAMM_CUDA_TRY(cudaStreamWaitEvent(st, hv.join, 0));
   return LRAMM_OK;
 }
 
