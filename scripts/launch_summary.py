@@ -4,7 +4,7 @@
 
 Lists every launch's kernel and duration, then per-kernel totals for one lramm step: the
 launches from the N-th occurrence of the step's first kernel (default: the sketch quantiser
-`absmax_rows_kernel`, second step) up to the next occurrence.
+`absmax_tile_kernel`, second step) up to the next occurrence.
 """
 import collections
 import csv
@@ -12,7 +12,7 @@ import re
 import sys
 
 path = sys.argv[1]
-first = re.compile(sys.argv[2] if len(sys.argv) > 2 else r"absmax_rows_kernel")
+first = re.compile(sys.argv[2] if len(sys.argv) > 2 else r"absmax_tile_kernel")
 lines = [l for l in open(path) if l.startswith('"')]
 rows = list(csv.DictReader(lines))
 launches = []
