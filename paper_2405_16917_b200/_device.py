@@ -5,6 +5,8 @@ from __future__ import annotations
 import ctypes
 from collections import OrderedDict
 
+import threading
+
 import numpy as np
 import torch
 
@@ -87,6 +89,7 @@ class OmegaCache:
         self.capacity = capacity
         self.host: OrderedDict = OrderedDict()
         self.dev: OrderedDict = OrderedDict()
+        self.lock = threading.RLock()  # host API callers may run on several threads
 
     @staticmethod
     def philox_key(seed: int, ncols: int, width: int):
@@ -100,6 +103,10 @@ class OmegaCache:
             table.popitem(last=False)
 
     def device_omega(self, seed: int, ncols: int, width: int, device: torch.device) -> torch.Tensor:
+        with self.lock:
+            return self._device_omega(seed, ncols, width, device)
+
+    def _device_omega(self, seed: int, ncols: int, width: int, device: torch.device) -> torch.Tensor:
         key = (int(seed), int(ncols), int(width), device.index)
         t = self.dev.get(key)
         if t is None:
@@ -110,12 +117,19 @@ class OmegaCache:
             ws = WORKSPACE.get(wsz, device)
             k0, k1 = self.philox_key(seed, ncols, width)
             N.check(N.LIB.lramm_omega(k0, k1, ncols, width, ptr(t), ptr(ws), wsz, stream_handle(device)))
+            if not torch.cuda.is_current_stream_capturing():
+                # consumers on other streams (the host C ABI's own streams) read it in place
+                torch.cuda.current_stream(device).synchronize()
             self._put(self.dev, key, t)
         else:
             self.dev.move_to_end(key)
         return t
 
     def host_omega(self, seed: int, ncols: int, width: int) -> np.ndarray:
+        with self.lock:
+            return self._host_omega(seed, ncols, width)
+
+    def _host_omega(self, seed: int, ncols: int, width: int) -> np.ndarray:
         key = (int(seed), int(ncols), int(width))
         pinned = self.host.get(key)
         if pinned is None:

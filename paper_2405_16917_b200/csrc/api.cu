@@ -96,10 +96,34 @@ struct HostCtx {
   int *status = nullptr;
   int dev = -1;
 };
-static HostCtx &host_ctx() {
-  static HostCtx c;
-  return c;
-}
+// Host entry points lease one context (streams + device buffer) for the duration of a call:
+// concurrent host threads run on their own contexts and streams (the reference's kernels are
+// thread-safe and reentrant and its sweeps call them from a thread pool, cli.py:415-419);
+// contexts are reused, so device memory stays bounded by the peak number of concurrent calls.
+struct CtxLease {
+  static std::mutex &mu() {
+    static std::mutex m;
+    return m;
+  }
+  static std::vector<HostCtx *> &pool() {
+    static std::vector<HostCtx *> p;
+    return p;
+  }
+  HostCtx *c;
+  CtxLease() {
+    std::lock_guard<std::mutex> g(mu());
+    if (pool().empty()) {
+      c = new HostCtx();
+    } else {
+      c = pool().back();
+      pool().pop_back();
+    }
+  }
+  ~CtxLease() {
+    std::lock_guard<std::mutex> g(mu());
+    pool().push_back(c);
+  }
+};
 static int host_reserve(HostCtx &c, size_t bytes) {
   int dev = 0;
   LRAMM_CUDA_TRY(cudaGetDevice(&dev));
@@ -289,8 +313,8 @@ static int finish(HostCtx &c) {
 
 int lramm_host_matmul(const double *a, const double *b, double *out, int64_t m, int64_t k, int64_t n) {
   if (m < 1 || k < 1 || n < 1) return fail(LRAMM_ERR_SHAPE, "inner dimensions differ");
-  HostCtx &c = host_ctx();
-  std::lock_guard<std::mutex> g(c.mu);
+  CtxLease lease;
+  HostCtx &c = *lease.c;
   size_t gw = dgemm_ws_bytes(0, m, n, k);
   size_t need = (size_t)round_up((m * k + k * n + m * n) * 8, 256) * 1 + gw + 4096;
   LRAMM_TRY(host_reserve(c, need));
@@ -334,8 +358,8 @@ int lramm_host_imatmul(const int32_t *a, const int32_t *b, int64_t *out, int64_t
   // into 1..4 8-bit limbs (as many as its largest magnitude needs) and the limb products run
   // on the int8 tensor cores, accumulated exactly in int64
   if (m < 1 || k < 1 || n < 1) return fail(LRAMM_ERR_SHAPE, "inner dimensions differ");
-  HostCtx &c = host_ctx();
-  std::lock_guard<std::mutex> g(c.mu);
+  CtxLease lease;
+  HostCtx &c = *lease.c;
   const int64_t ldk = round_up(k, 16);
   size_t need = (size_t)round_up((m * k + 2 * k * n) * 4, 256) + round_up(4 * (m + n) * ldk, 256) +
                 round_up(2 * m * n * 8, 256) + 8192;
@@ -373,8 +397,8 @@ int lramm_host_imatmul(const int32_t *a, const int32_t *b, int64_t *out, int64_t
 
 int lramm_host_scale_round_clip(const double *a, int64_t m, int64_t n, double scale, int cap, int32_t *out) {
   if (m < 1 || n < 1) return fail(LRAMM_ERR_SHAPE, "empty matrix");
-  HostCtx &c = host_ctx();
-  std::lock_guard<std::mutex> g(c.mu);
+  CtxLease lease;
+  HostCtx &c = *lease.c;
   LRAMM_TRY(host_reserve(c, (size_t)round_up(m * n * 8, 256) + round_up(m * n * 4, 256) + 4096));
   Arena ar(c.buf, c.cap);
   double *da = ar.take<double>(m * n);
@@ -388,8 +412,8 @@ int lramm_host_scale_round_clip(const double *a, int64_t m, int64_t n, double sc
 
 int lramm_host_svd(const double *a, int64_t m, int64_t n, double *u, double *s, double *v) {
   if (m < 1 || n < 1) return fail(LRAMM_ERR_SHAPE, "empty matrix");
-  HostCtx &c = host_ctx();
-  std::lock_guard<std::mutex> g(c.mu);
+  CtxLease lease;
+  HostCtx &c = *lease.c;
   const int64_t t = std::min(m, n);
   size_t ws = lramm_svd_ws(m, n);
   LRAMM_TRY(host_reserve(c, (size_t)round_up((m * n + m * t + t + n * t) * 8, 256) + ws + 8192));
@@ -415,8 +439,8 @@ int lramm_host_lramm(const void *a, const void *b, int in_dtype, int64_t m, int6
                      int c_dtype, void *d, int d_dtype, lramm_timings_t *timings) {
   if (!params) return fail(LRAMM_ERR_PARAM, "lramm: params is NULL");
   if (in_dtype != LRAMM_F32 && in_dtype != LRAMM_F64) return fail(LRAMM_ERR_PARAM, "inputs must be F32 or F64");
-  HostCtx &c = host_ctx();
-  std::lock_guard<std::mutex> g(c.mu);
+  CtxLease lease;
+  HostCtx &c = *lease.c;
   const int64_t es = in_dtype == LRAMM_F32 ? 4 : 8, ds = d_dtype == LRAMM_F32 ? 4 : 8,
                 cs = c_dtype == LRAMM_F32 ? 4 : 8;
   const int64_t wa = std::min<int64_t>(params->rank + params->oversample, std::min(m, k));
