@@ -347,11 +347,65 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // stand-alone epilogue over an int32 accumulator matrix (after split-K)
-__global__ void epilogue_kernel(const int32_t *__restrict__ acc, int64_t M, int64_t N, int64_t lda, EpiDev epi) {
-  int64_t n = M * N;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i / N, c = i - r * N;
-    epi_store(epi, acc[r * lda + c], r, c);
+// dequantised value of one int32 accumulator: acc / (rs cs) correctly rounded through the
+// reciprocal + exact residual check (div_exact; __ddiv_rn for a non-normal scale product)
+__device__ __forceinline__ double epi_dequant_fast(const EpiDev &e, int32_t acc, int64_t row, int64_t col) {
+  const double rs = e.row_scale ? e.row_scale[row * e.row_scale_inc] : 1.0;
+  const double cs = e.col_scale ? e.col_scale[col * e.col_scale_inc] : 1.0;
+  const double sc = __dmul_rn(rs, cs);
+  const double v = (sc >= 2.2250738585072014e-308 && sc <= 1.7976931348623157e308)
+                       ? div_exact((double)acc, sc, __drcp_rn(sc))
+                       : __ddiv_rn((double)acc, sc);
+  return epi_alpha_beta(e, v, row, col);
+}
+
+// int32 outputs (raw copy / accumulate) of lramm_dequant: the generic per-element store
+__global__ void epilogue_generic_kernel(const int32_t *__restrict__ acc, int64_t M, int64_t N, int64_t lda,
+                                        EpiDev epi) {
+  for (int64_t r = blockIdx.y; r < M; r += gridDim.y)
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < N; c += (int64_t)gridDim.x * blockDim.x)
+      epi_store(epi, acc[r * lda + c], r, c);
+}
+
+// split-K epilogue (int32 accumulator -> dequantised f32 / f64): a warp per row, lanes over the
+// columns (no 64-bit index division); transposed outputs go through a 32 x 32
+// shared-memory tile so both the accumulator reads and the output writes are coalesced
+template <bool TRANS>
+__global__ void __launch_bounds__(256) epilogue_kernel(const int32_t *__restrict__ acc, int64_t M, int64_t N,
+                                                       int64_t lda, EpiDev epi) {
+  if constexpr (!TRANS) {
+    // one warp per row, lanes over the columns (every lane busy for any N >= 32)
+    const int lane = threadIdx.x & 31;
+    const int64_t wstep = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < M; r += wstep)
+      for (int64_t c = lane; c < N; c += 32) {
+        const double v = epi_dequant_fast(epi, acc[r * lda + c], r, c);
+        if (epi.out_dtype == LRAMM_F64)
+          ((double *)epi.out)[r * epi.ldo + c] = v;
+        else
+          ((float *)epi.out)[r * epi.ldo + c] = __double2float_rn(v);
+      }
+  } else {
+    __shared__ double t[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int64_t r0 = (int64_t)blockIdx.y * 32; r0 < M; r0 += (int64_t)gridDim.y * 32)
+      for (int64_t c0 = (int64_t)blockIdx.x * 32; c0 < N; c0 += (int64_t)gridDim.x * 32) {
+        for (int rr = ty; rr < 32; rr += 8) {
+          const int64_t r = r0 + rr, c = c0 + tx;
+          t[rr][tx] = (r < M && c < N) ? epi_dequant_fast(epi, acc[r * lda + c], r, c) : 0.0;
+        }
+        __syncthreads();
+        for (int cc = ty; cc < 32; cc += 8) {
+          const int64_t c = c0 + cc, r = r0 + tx;
+          if (r < M && c < N) {
+            if (epi.out_dtype == LRAMM_F64)
+              ((double *)epi.out)[c * epi.ldo + r] = t[tx][cc];
+            else
+              ((float *)epi.out)[c * epi.ldo + r] = __double2float_rn(t[tx][cc]);
+          }
+        }
+        __syncthreads();
+      }
   }
 }
 
@@ -549,8 +603,18 @@ int split_limbs_device(const int32_t *src, int64_t rows, int64_t cols, int64_t l
 
 int epilogue_device(const int32_t *acc, int64_t M, int64_t N, int64_t lda, const lramm_epilogue_t &epi,
                     cudaStream_t st) {
-  int grid = (int)std::min<int64_t>(ceil_div(M * N, 256), 16LL * num_sms());
-  epilogue_kernel<<<grid, 256, 0, st>>>(acc, M, N, lda, to_dev(epi));
+  if (epi.out_dtype != LRAMM_F64 && epi.out_dtype != LRAMM_F32) {
+    const dim3 grid((unsigned)ceil_div(N, 256),
+                    (unsigned)std::min<int64_t>(M, std::max<int64_t>(1, 16LL * num_sms() / ceil_div(N, 256))));
+    epilogue_generic_kernel<<<grid, 256, 0, st>>>(acc, M, N, lda, to_dev(epi));
+  } else if (epi.transpose_out) {
+    const dim3 grid((unsigned)std::min<int64_t>(ceil_div(N, 32), 4096),
+                    (unsigned)std::min<int64_t>(ceil_div(M, 32), std::max<int64_t>(1, 8LL * num_sms() / ceil_div(N, 32))));
+    epilogue_kernel<true><<<grid, 256, 0, st>>>(acc, M, N, lda, to_dev(epi));
+  } else {
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(M, 8), 16LL * num_sms());
+    epilogue_kernel<false><<<grid, 256, 0, st>>>(acc, M, N, lda, to_dev(epi));
+  }
   LRAMM_LAUNCH_CHECK();
   return LRAMM_OK;
 }
