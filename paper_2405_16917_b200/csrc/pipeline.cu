@@ -40,7 +40,7 @@ int dgemm_device(int trans_a, int64_t M, int64_t N, int64_t K, const double *A, 
                  int64_t ldb, double *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st);
 size_t dgemm_ws_bytes(int trans_a, int64_t M, int64_t N, int64_t K);
 int qr_device(const double *y, int64_t m, int64_t w, int64_t ldy, double *q, int64_t ldq, double *r, void *ws,
-              size_t ws_bytes, cudaStream_t st, bool q_needed = true);
+              size_t ws_bytes, cudaStream_t st, bool q_needed = true, bool fast = false);
 size_t qr_ws_bytes(int64_t m, int64_t w);
 int svd_tall_pside_device(const double *T, int64_t m, int64_t n, int64_t ldt, const double *s, const double *H,
                           int64_t ldh, double *pside, int64_t ldp, int *status, void *ws, size_t ws_bytes,
@@ -331,7 +331,7 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
     }
     LRAMM_TRY(dgemm_device(0, rows, w, cols, x64, cols, omega, w, b.Y, w, b.gemm_ws, b.gemm_bytes, st));
   }
-  LRAMM_TRY(qr_device(b.Y, rows, w, w, b.Q, w, nullptr, b.qr_ws, b.qr_bytes, st));
+  LRAMM_TRY(qr_device(b.Y, rows, w, w, b.Q, w, nullptr, b.qr_ws, b.qr_bytes, st, true, b.fast));
   if (b.fast && P.power_iters > 0) LRAMM_TRY(join_helper());
   for (int it = 0; it < P.power_iters; ++it) {
     // Z = X^T Q ; Qz = qr(Z) ; Y = X Qz ; Q = qr(Y)   (rsvd.py:60-64)
@@ -341,14 +341,14 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
     } else {
       LRAMM_TRY(dgemm_device(1, cols, w, rows, x64, cols, b.Q, w, b.Z, w, b.gemm_ws, b.gemm_bytes, st));
     }
-    LRAMM_TRY(qr_device(b.Z, cols, w, w, b.Qz, w, nullptr, b.qr_ws, b.qr_bytes, st));
+    LRAMM_TRY(qr_device(b.Z, cols, w, w, b.Qz, w, nullptr, b.qr_ws, b.qr_bytes, st, true, b.fast));
     if (b.fast) {
       LRAMM_TRY(quant(b.Qz, LRAMM_F64, cols, w, w, P.power_bits, gran_r, 1, b.qzq, nullptr, b.qz_ws, b.qz_bytes, st));
       LRAMM_TRY(qprod(b.xr_p, b.qzq, rows, w, cols, b.Y, w, 0, b.acc, st));
     } else {
       LRAMM_TRY(dgemm_device(0, rows, w, cols, x64, cols, b.Qz, w, b.Y, w, b.gemm_ws, b.gemm_bytes, st));
     }
-    LRAMM_TRY(qr_device(b.Y, rows, w, w, b.Q, w, nullptr, b.qr_ws, b.qr_bytes, st));
+    LRAMM_TRY(qr_device(b.Y, rows, w, w, b.Q, w, nullptr, b.qr_ws, b.qr_bytes, st, true, b.fast));
   }
   // Bs^T = X^T Q   (rsvd.py:77, evaluated transposed)
   if (b.fast) {
