@@ -85,8 +85,11 @@ def test_rsvd_exact_rank_one(L):
     assert np.linalg.norm(a - (f.u * f.sigma) @ f.v.T) <= 1e-8
 
 
-def test_rsvd_fast_mode_matches_restatement(L):
-    x = O.synth(512, 384, "exp:24", 6, 0, 0)
+@pytest.mark.parametrize("spectrum", ["exp:24", "poly:1.5", "poly:3"])
+def test_rsvd_fast_mode_matches_restatement(L, spectrum):
+    # exp:24 keeps every sketch well conditioned (single CholeskyQR pass in fast mode); the
+    # polynomial spectra push kappa(Y) past the second-pass threshold
+    x = O.synth(512, 384, spectrum, 6, 0, 0)
     for gran in ("tensor", "row"):
         spec = O.SketchSpec(8, 8, 8, gran)
         f_ref = O.rsvd(x, 32, 1, 8, 123, spec)
