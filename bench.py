@@ -611,8 +611,14 @@ def stage_rooflines(per, reps, cfg, peaks, sweeps=10):
     prods += [(r, r, k, 8), (r, n, r, 8), (m, n, r, 4)]
     g_ops = sum(2.0 * M * N * K for M, N, K, _ in prods)
     g_bytes = sum(M * K + N * K + M * N * ob for M, N, K, ob in prods)
-    qr_rows = [m] * (1 + q) + [k] * q + [k] + [k] * (1 + q) + [n] * q + [n]
-    qr_flops = sum(6.0 * rr * w * w for rr in qr_rows) + 2.0 * (m + k) * w * w + 2.0 * (k + n) * w * w
+    # one CholeskyQR pass = Gram (2 rows w^2, full) + TRSM (rows w^2); parity mode and the SVD's
+    # projection always run the second pass, fast-mode sketches only when kappa(Y) > ~95:
+    # the minimum (one pass for fast-mode sketches) is the algorithmic work counted here
+    sk_rows = [m] * (1 + q) + [k] * q + [k] * (1 + q) + [n] * q
+    pj_rows = [k, n]
+    passes = 1 if cfg.get("mode") == "fast" else 2
+    qr_flops = (sum(3.0 * passes * rr * w * w for rr in sk_rows) + sum(6.0 * rr * w * w for rr in pj_rows)
+                + 2.0 * (m + k) * w * w + 2.0 * (k + n) * w * w)
     jac_flops = 2 * sweeps * (w * (w - 1) / 2) * 8 * w
     work = {
         "omega": (0.0, 8.0 * (k + n) * w, "bytes: Omega_A, Omega_B written (fp64)"),
@@ -620,7 +626,8 @@ def stage_rooflines(per, reps, cfg, peaks, sweeps=10):
                                          "recombination operands read + int8 written"),
         "int8_gemm": (g_ops / int8, float(g_bytes), "2MNK over the sketch/projection/recombination products; "
                                                    "int8 operands read + outputs written"),
-        "fp64_qr": (qr_flops / fp64, 0.0, "6 rows w^2 per CholeskyQR2 + the two lifts (fp64 tensor peak)"),
+        "fp64_qr": (qr_flops / fp64, 0.0, "3 rows w^2 per CholeskyQR pass (one pass for fast-mode sketches, two "
+                                          "for the projections) + the two lifts (fp64 tensor peak)"),
         "jacobi_svd": (jac_flops / fp64, 0.0, f"{sweeps} sweeps x w(w-1)/2 pairs x 8w flops, two operands"),
     }
     out = {}
