@@ -13,6 +13,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -527,7 +528,13 @@ int igemm_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, 
   const int BN = pick_bn(N);
   const int stage_bytes = BM * BK + BN * BK;
   // no more stages than k-blocks: short-K products (E2, E3) then fit two CTAs per SM
-  const int stages = std::max(2, std::min(std::min(8, kb_total), (kSmemBudget - 2048) / stage_bytes));
+  int stages = std::max(2, std::min(std::min(8, kb_total), (kSmemBudget - 2048) / stage_bytes));
+  // more than one wave: a shallower ring that fits two CTAs per SM (and two TMEM accumulators),
+  // so one CTA's epilogue overlaps the other's loads and MMAs (c5 E3 131072x8192x1024: 4.1 ->
+  // 2.7 ms; c3 E3: 239 -> 143 us); single-wave grids keep the deep ring
+  const int64_t ctas = ceil_div(M, BM) * ceil_div(N, BN) * split_k;
+  const int two_per_sm = (113 * 1024 - 2048) / stage_bytes;
+  if (ctas > num_sms() && two_per_sm >= 2) stages = std::min(stages, two_per_sm);
   const int smem = stages * stage_bytes + (2 * stages + 2) * 8 + 1024 + 64;
   CUtensorMap ta, tb;
   LRAMM_TRY(make_tmap_i8(&ta, a, M, K, lda, BM));
