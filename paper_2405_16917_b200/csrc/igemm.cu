@@ -34,6 +34,7 @@ struct EpiDev {
   int64_t ldc;
   int shift;  // EK_I64_ADD: out += acc * 2^shift (limb-pair products of multi-limb operands)
   int signs;  // bit 0: A int8 signed, bit 1: B int8 signed (unsigned limbs otherwise)
+  int nfast;  // grid laid out with N tiles fastest (see igemm_device)
 };
 
 // Correctly rounded a / s for |a| < 2^53 integer-valued a and normal s > 0, given y = RN(1/s):
@@ -136,8 +137,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int64_t n0 = (int64_t)blockIdx.y * BN;
+  // tile order: blockIdx.x runs over N tiles when the grid was laid out N-fastest (nfast), so
+  // consecutive CTAs share the A tile and the (smaller) B operand is what gets re-read
+  const bool nfast = epi.nfast != 0;
+  const int64_t m0 = (int64_t)(nfast ? blockIdx.y : blockIdx.x) * BM;
+  const int64_t n0 = (int64_t)(nfast ? blockIdx.x : blockIdx.y) * BN;
   const int kb_total = (int)((K + BK - 1) / BK);
   const int kb0 = blockIdx.z * kb_per_split;
   const int kb1 = min(kb0 + kb_per_split, kb_total);
@@ -494,6 +498,7 @@ EpiDev to_dev(const lramm_epilogue_t &e) {
   d.ldc = e.ldc;
   d.shift = 0;
   d.signs = 3;
+  d.nfast = 0;
   return d;
 }
 
@@ -558,10 +563,17 @@ int igemm_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, 
 #undef LRAMM_IG_PICK
   if (!kern) return fail(LRAMM_ERR_PARAM, "igemm: unsupported epilogue");
   LRAMM_CUDA_TRY(allow_max_dyn_smem(kern));
-  dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(N, BN), (unsigned)split_k);
+  // rasterisation: M-fastest keeps one B tile hot while A tiles stream; when A is the larger
+  // operand and does not fit in L2 (c5: A 134 MB-1 GB, B 8 MB) that re-reads A from HBM once per
+  // N tile, so the grid goes N-fastest instead and B is the operand re-read (from L2)
+  const int64_t mt = ceil_div(M, BM), nt = ceil_div(N, BN);
+  const bool nfast = nt > 1 && M * K > N * K && M * K > (int64_t)48 << 20 && mt <= 65535;
+  dim3 grid = nfast ? dim3((unsigned)nt, (unsigned)mt, (unsigned)split_k)
+                    : dim3((unsigned)mt, (unsigned)nt, (unsigned)split_k);
   EpiDev ed = to_dev(epi);
   ed.shift = g_limb_shift;
   ed.signs = g_limb_signs;
+  ed.nfast = nfast ? 1 : 0;
   kern<<<grid, kThreads, smem, st>>>(ta, tb, M, N, K, BN, stages, kb_per, ed);
   LRAMM_LAUNCH_CHECK();
   return LRAMM_OK;
