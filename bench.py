@@ -296,7 +296,7 @@ def run_ours(args, cfg, world, rank, local):
     import paper_2405_16917_b200 as L
 
     P = pairs_per_rank(cfg, world)
-    S = min(P, cfg.get("streams", 1))
+    S = min(P, int(os.environ.get("BENCH_STREAMS", cfg.get("streams", 1))))
     pairs = [synth_pair(cfg, rank * P + j, dev) for j in range(P)]
     a, b = pairs[0]
     params = L.LrammParams(rank=cfg["rank"], bits=tuple(cfg["bits"]), power_iters=cfg["power_iters"],
