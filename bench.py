@@ -40,7 +40,7 @@ CONFIGS = {
     # BASELINE.json configs[3]: 64 independent 2048^3 pairs, r=128, p=10, q=0 (reference default),
     # int8 sketches with the reference's per-tensor quantiser; batch sharded across ranks
     "c4": dict(m=2048, k=2048, n=2048, rank=128, oversample=10, power_iters=0, bits=(8, 8, 8), tau=64.0,
-               mode="fast", sketch_bits=8, power_bits=8, proj_bits=8, granularity="tensor", pairs=64, streams=16),
+               mode="fast", sketch_bits=8, power_bits=8, proj_bits=8, granularity="tensor", pairs=64, streams=8),
     # BASELINE.json configs[0] (the reference's CPU-runnable case), for quick runs
     "c1": dict(m=1024, k=1024, n=1024, rank=64, oversample=10, power_iters=1, bits=(8, 8, 8), tau=32.0,
                mode="fast", sketch_bits=8, power_bits=8, proj_bits=8, granularity="row"),
