@@ -46,7 +46,7 @@ int quantize_device(const void *, int, int64_t, int64_t, int64_t, int, int, int,
                     void *, size_t, cudaStream_t);
 size_t quantize_ws_bytes(int64_t, int64_t);
 int quantize_pair_device(const void *, int, int64_t, int64_t, int64_t, int, int, int8_t *, int64_t, double *, int, int,
-                         int8_t *, int64_t, double *, int *, void *, size_t, cudaStream_t);
+                         int8_t *, int64_t, double *, int *, void *, size_t, cudaStream_t, int r_packed = 0);
 int absmax_device(const void *, int, int64_t, int64_t, int64_t, int, double *, int *, cudaStream_t);
 int quantize_amax_device(const void *, int, int64_t, int64_t, int64_t, int, int, int, const double *, void *, int, int64_t,
                          double *, cudaStream_t);
@@ -56,7 +56,7 @@ size_t cholqr_pass_ws_bytes(int64_t, int64_t);
 int epilogue_device(const int32_t *, int64_t, int64_t, int64_t, const lramm_epilogue_t &, cudaStream_t);
 int scale_round_clip_device(const double *, int64_t, int64_t, int64_t, double, int, int32_t *, int64_t, cudaStream_t);
 int igemm_device(int64_t, int64_t, int64_t, const int8_t *, int64_t, const int8_t *, int64_t, const lramm_epilogue_t &,
-                 int, cudaStream_t);
+                 int, cudaStream_t, int a4 = 0);
 int dgemm_device(int, int64_t, int64_t, int64_t, const double *, int64_t, const double *, int64_t, double *, int64_t,
                  void *, size_t, cudaStream_t);
 size_t dgemm_ws_bytes(int, int64_t, int64_t, int64_t);

@@ -35,6 +35,7 @@ struct EpiDev {
   int shift;  // EK_I64_ADD: out += acc * 2^shift (limb-pair products of multi-limb operands)
   int signs;  // bit 0: A int8 signed, bit 1: B int8 signed (unsigned limbs otherwise)
   int nfast;  // grid laid out with N tiles fastest (see igemm_device)
+  int a4;     // A arrives as packed int4 (two's-complement nibbles) and is unpacked to int8 in smem
 };
 
 // Correctly rounded a / s for |a| < 2^53 integer-valued a and normal s > 0, given y = RN(1/s):
@@ -129,11 +130,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t a_bytes = BM * BK;
   const uint32_t b_bytes = (uint32_t)BN * BK;
+  const bool a4 = epi.a4 != 0;
+  const uint32_t a4_bytes = a4 ? BM * (BK / 2) : 0u;  // packed staging tile (64 B per row, no swizzle)
   uint8_t *sA = smem;
   uint8_t *sB = smem + (size_t)stages * a_bytes;
-  uint64_t *full = reinterpret_cast<uint64_t *>(sB + (size_t)stages * b_bytes);
+  uint8_t *sA4 = sB + (size_t)stages * b_bytes;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sA4 + (size_t)stages * a4_bytes);
   uint64_t *empty = full + stages;
-  uint64_t *tmem_full = empty + stages;
+  uint64_t *unpacked = empty + stages;  // a4: the int8 A tile of the stage is in sA
+  uint64_t *tmem_full = unpacked + stages;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -154,6 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < stages; ++s) {
       sm100::mbar_init(&full[s], 1);
       sm100::mbar_init(&empty[s], 1);
+      sm100::mbar_init(&unpacked[s], 256);  // every epilogue thread unpacks a quarter of a row band
     }
     sm100::mbar_init(tmem_full, 1);
     sm100::fence_barrier_init();
@@ -170,9 +176,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = i % stages;
         const uint32_t ph = (uint32_t)(i / stages) & 1u;
         sm100::mbar_wait(&empty[s], ph ^ 1u);
-        sm100::mbar_arrive_expect_tx(&full[s], a_bytes + b_bytes);
+        sm100::mbar_arrive_expect_tx(&full[s], (a4 ? a4_bytes : a_bytes) + b_bytes);
         const int32_t kx = (kb0 + i) * BK;
-        sm100::tma_load_2d(&tma_a, &full[s], sA + (size_t)s * a_bytes, kx, (int32_t)m0);
+        if (a4)
+          sm100::tma_load_2d(&tma_a, &full[s], sA4 + (size_t)s * a4_bytes, kx / 2, (int32_t)m0);
+        else
+          sm100::tma_load_2d(&tma_a, &full[s], sA + (size_t)s * a_bytes, kx, (int32_t)m0);
         sm100::tma_load_2d(&tma_b, &full[s], sB + (size_t)s * b_bytes, kx, (int32_t)n0);
       }
     }
@@ -183,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < nkb; ++i) {
         const int s = i % stages;
         const uint32_t ph = (uint32_t)(i / stages) & 1u;
-        sm100::mbar_wait(&full[s], ph);
+        sm100::mbar_wait(a4 ? &unpacked[s] : &full[s], ph);
         sm100::tc_fence_after();
         const uint64_t ad = sm100::sdesc_k_sw128(sm100::smem_u32(sA + (size_t)s * a_bytes));
         const uint64_t bd = sm100::sdesc_k_sw128(sm100::smem_u32(sB + (size_t)s * b_bytes));
@@ -205,6 +214,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int etid = threadIdx.x - 64;     // 0..255
     const int rloc = quarter * 32 + lane;
     const int64_t row = m0 + rloc;
+    if (a4) {
+      // mainloop role of the epilogue warps: unpack each stage's packed A tile (BM rows x 64 B of
+      // nibbles) into the int8 tile the MMA reads, in the TMA SWIZZLE_128B layout (16-byte chunk c
+      // of row r at chunk c ^ (r & 7)); one 16-byte chunk = 8 packed bytes per step
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % stages;
+        sm100::mbar_wait(&full[s], (uint32_t)(i / stages) & 1u);
+        const uint8_t *src = sA4 + (size_t)s * a4_bytes;
+        uint8_t *dst = sA + (size_t)s * a_bytes;
+#pragma unroll
+        for (int t = 0; t < (BM * 8) / 256; ++t) {
+          const int idx = etid + 256 * t, r = idx >> 3, c = idx & 7;
+          const uint2 pk = *reinterpret_cast<const uint2 *>(src + r * (BK / 2) + 8 * c);
+          uint32_t w[4];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t v = h ? pk.y : pk.x;  // 4 packed bytes -> 8 int8 (2 words)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const uint32_t b2 = v >> (16 * q);  // two packed bytes -> four nibbles
+              uint32_t out = 0;
+#pragma unroll
+              for (int n = 0; n < 4; ++n) {
+                const int32_t nib = (int32_t)((b2 >> (4 * n)) & 0xF);
+                out |= (uint32_t)(uint8_t)(int8_t)((nib ^ 8) - 8) << (8 * n);
+              }
+              w[2 * h + q] = out;
+            }
+          }
+          *reinterpret_cast<uint4 *>(dst + r * BK + ((c ^ (r & 7)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        sm100::fence_proxy_async_smem();  // generic stores -> the tensor core's async-proxy reads
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm100::smem_u32(&unpacked[s])) : "memory");
+      }
+    }
     if (nkb > 0) {
       sm100::mbar_wait(tmem_full, 0);
       sm100::tc_fence_after();
@@ -480,6 +524,22 @@ int make_tmap_i8(CUtensorMap *m, const int8_t *ptr, int64_t rows, int64_t k, int
   return LRAMM_OK;
 }
 
+// packed-int4 A: rows of ceil(K/2) bytes, box 64 bytes (one 128-element k-block) x box_rows,
+// no swizzle (the kernel's unpack step writes the swizzled int8 tile)
+int make_tmap_i4(CUtensorMap *m, const int8_t *ptr, int64_t rows, int64_t k, int64_t ld_bytes, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(LRAMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)ceil_div(k, 2), (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)(BK / 2), (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t *>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LRAMM_ERR_CUDA, "cuTensorMapEncodeTiled (int4) failed (%d)", (int)r);
+  return LRAMM_OK;
+}
+
 EpiDev to_dev(const lramm_epilogue_t &e) {
   EpiDev d;
   d.out_dtype = e.out_dtype;
@@ -499,6 +559,7 @@ EpiDev to_dev(const lramm_epilogue_t &e) {
   d.shift = 0;
   d.signs = 3;
   d.nfast = 0;
+  d.a4 = 0;
   return d;
 }
 
@@ -517,10 +578,11 @@ int pick_bn(int64_t N) {
 }
 
 int igemm_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, const int8_t *b, int64_t ldb,
-                 const lramm_epilogue_t &epi, int split_k, cudaStream_t st) {
+                 const lramm_epilogue_t &epi, int split_k, cudaStream_t st, int a4 = 0) {
   if (M < 1 || N < 1 || K < 1) return fail(LRAMM_ERR_SHAPE, "igemm: empty shape");
-  if (lda < K || ldb < K || (lda % 16) || (ldb % 16))
-    return fail(LRAMM_ERR_SHAPE, "igemm: leading dims must be >= K and multiples of 16");
+  // a4: A is packed int4, lda in bytes (>= ceil(K/2))
+  if ((a4 ? 2 * lda < K : lda < K) || ldb < K || (lda % 16) || (ldb % 16))
+    return fail(LRAMM_ERR_SHAPE, "igemm: leading dims must cover K and be multiples of 16");
   if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15)
     return fail(LRAMM_ERR_SHAPE, "igemm: operands must be 16-byte aligned");
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return fail(LRAMM_ERR_SHAPE, "igemm: dims exceed int32");
@@ -531,7 +593,7 @@ int igemm_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, 
   const int kb_per = (int)ceil_div(kb_total, split_k);
   split_k = (int)ceil_div(kb_total, kb_per);
   const int BN = pick_bn(N);
-  const int stage_bytes = BM * BK + BN * BK;
+  const int stage_bytes = BM * BK + BN * BK + (a4 ? BM * BK / 2 : 0);
   // no more stages than k-blocks: short-K products (E2, E3) then fit two CTAs per SM
   int stages = std::max(2, std::min(std::min(8, kb_total), (kSmemBudget - 2048) / stage_bytes));
   // more than one wave: a shallower ring that fits two CTAs per SM (and two TMEM accumulators),
@@ -540,9 +602,12 @@ int igemm_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, 
   const int64_t ctas = ceil_div(M, BM) * ceil_div(N, BN) * split_k;
   const int two_per_sm = (113 * 1024 - 2048) / stage_bytes;
   if (ctas > num_sms() && two_per_sm >= 2) stages = std::min(stages, two_per_sm);
-  const int smem = stages * stage_bytes + (2 * stages + 2) * 8 + 1024 + 64;
+  const int smem = stages * stage_bytes + (3 * stages + 2) * 8 + 1024 + 64;
   CUtensorMap ta, tb;
-  LRAMM_TRY(make_tmap_i8(&ta, a, M, K, lda, BM));
+  if (a4)
+    LRAMM_TRY(make_tmap_i4(&ta, a, M, K, lda, BM));
+  else
+    LRAMM_TRY(make_tmap_i8(&ta, a, M, K, lda, BM));
   LRAMM_TRY(make_tmap_i8(&tb, b, N, K, ldb, BN));
   const int ek = epi.out_dtype == LRAMM_I64 ? EK_I64_ADD
                  : epi.out_dtype == LRAMM_I32 ? (epi.accumulate ? EK_I32_ATOMIC : EK_I32)
@@ -574,6 +639,7 @@ int igemm_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, 
   ed.shift = g_limb_shift;
   ed.signs = g_limb_signs;
   ed.nfast = nfast ? 1 : 0;
+  ed.a4 = a4 ? 1 : 0;
   kern<<<grid, kThreads, smem, st>>>(ta, tb, M, N, K, BN, stages, kb_per, ed);
   LRAMM_LAUNCH_CHECK();
   return LRAMM_OK;

@@ -25,14 +25,15 @@ int quantize_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int6
 size_t quantize_ws_bytes(int64_t rows, int64_t cols);
 int quantize_pair_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits_r, int gran_r,
                          int8_t *qr, int64_t ldqr, double *scales_r, int bits_t, int gran_t, int8_t *qt, int64_t ldqt,
-                         double *scales_t, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st);
+                         double *scales_t, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st,
+                         int r_packed = 0);
 int igemm_limbs_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, int64_t pa, int la,
                        const int8_t *b, int64_t ldb, int64_t pb, int lb, int64_t *acc64,
                        const lramm_epilogue_t &epi, cudaStream_t st);
 int split_limbs_device(const int32_t *src, int64_t rows, int64_t cols, int64_t lds, int nlimb, int8_t *dst,
                        int64_t ldd, cudaStream_t st);
 int igemm_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, const int8_t *b, int64_t ldb,
-                 const lramm_epilogue_t &epi, int split_k, cudaStream_t st);
+                 const lramm_epilogue_t &epi, int split_k, cudaStream_t st, int a4 = 0);
 int epilogue_device(const int32_t *acc, int64_t M, int64_t N, int64_t lda, const lramm_epilogue_t &epi,
                     cudaStream_t st);
 int pick_bn(int64_t N);
@@ -89,6 +90,7 @@ struct QOp {  // a quantised K-major operand (bit budgets > 8: `limbs` 8-bit pla
   int limbs = 1;
   int64_t plane = 0;  // bytes between limb planes
   int64_t rows = 0;
+  int packed = 0;  // bit budgets <= 4 of the sketch's X: packed int4 (ld in bytes), unpacked in the GEMM
 };
 
 // 8-bit limbs needed for a bit budget: 1 (<= 8, the plain signed int8), 2 (<= 16), 3 (<= 24)
@@ -134,7 +136,12 @@ RsvdBufs carve_rsvd(Arena &ar, int64_t rows, int64_t cols, int x_dtype, const lr
   const bool row = b.gran == LRAMM_GRAN_ROW;
   const int64_t w = b.w;
   if (b.fast) {
-    b.xr_s = take_qop(ar, rows, cols, row ? rows : 1);
+    if (P.sketch_bits <= 4) {  // the sketch operand X stays packed int4 in HBM (half the bytes)
+      b.xr_s = take_qop(ar, rows, ceil_div(cols, 2), row ? rows : 1);
+      b.xr_s.packed = 1;
+    } else {
+      b.xr_s = take_qop(ar, rows, cols, row ? rows : 1);
+    }
     if (P.power_iters > 0) b.xr_p = P.power_bits == P.sketch_bits ? b.xr_s : take_qop(ar, rows, cols, row ? rows : 1);
     b.xc_j = take_qop(ar, cols, rows, row ? cols : 1);
     if (P.power_iters > 0) b.xc_p = P.power_bits == P.proj_bits ? b.xc_j : take_qop(ar, cols, rows, row ? cols : 1);
@@ -197,22 +204,22 @@ int qprod(const QOp &A, const QOp &B, int64_t M, int64_t N, int64_t K, double *C
   if (acc && tiles * 2 <= num_sms() && kb >= 8) split = (int)std::min<int64_t>(kb / 4, num_sms() / tiles);
   static const int split_env = getenv("LRAMM_QPROD_SPLIT") ? atoi(getenv("LRAMM_QPROD_SPLIT")) : 0;
   if (split_env > 0 && acc) split = (int)std::min<int64_t>(split_env, kb);
-  if (split <= 1) return igemm_device(M, N, K, A.q, A.ld, B.q, B.ld, e, 1, st);
+  if (split <= 1) return igemm_device(M, N, K, A.q, A.ld, B.q, B.ld, e, 1, st, A.packed);
   LRAMM_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)M * N * sizeof(int32_t), st));
   lramm_epilogue_t ea = {};
   ea.out_dtype = LRAMM_I32;
   ea.accumulate = 1;
   ea.out = acc;
   ea.ldo = N;
-  LRAMM_TRY(igemm_device(M, N, K, A.q, A.ld, B.q, B.ld, ea, split, st));
+  LRAMM_TRY(igemm_device(M, N, K, A.q, A.ld, B.q, B.ld, ea, split, st, A.packed));
   return epilogue_device(acc, M, N, N, e, st);
 }
 
 int quant(const void *x, int dtype, int64_t rows, int64_t cols, int64_t ldx, int bits, int gran, int transpose,
           QOp &o, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st, int32_t *tmp32 = nullptr) {
   if (o.limbs <= 1)
-    return quantize_device(x, dtype, rows, cols, ldx, bits, gran, transpose, o.q, LRAMM_I8, o.ld, o.scale, nonfinite,
-                           ws, ws_bytes, st);
+    return quantize_device(x, dtype, rows, cols, ldx, bits, gran, transpose, o.q, o.packed ? LRAMM_I4 : LRAMM_I8, o.ld,
+                           o.scale, nonfinite, ws, ws_bytes, st);
   // bit budgets > 8: the reference's integers (int32, bit-exact) -> 8-bit limb planes
   if (!tmp32) return fail(LRAMM_ERR_WORKSPACE, "quant: multi-limb operand needs an int32 staging buffer");
   const int64_t orows = transpose ? cols : rows, kdim = transpose ? rows : cols;
@@ -317,7 +324,7 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
     if (pair)
       LRAMM_TRY(quantize_pair_device(x, x_dtype, rows, cols, cols, P.sketch_bits, gran_l, b.xr_s.q, b.xr_s.ld,
                                      b.xr_s.scale, bits_first, gran_c, xc_first.q, xc_first.ld, xc_first.scale,
-                                     b.nonfinite, b.qz_ws, b.qz_bytes, st));
+                                     b.nonfinite, b.qz_ws, b.qz_bytes, st, b.xr_s.packed));
     else
       LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.sketch_bits, gran_l, 0, b.xr_s, b.nonfinite, b.qz_ws, b.qz_bytes,
                       st));

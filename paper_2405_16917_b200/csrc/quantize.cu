@@ -126,9 +126,10 @@ __global__ void __launch_bounds__(256, 4) absmax_tile_kernel(const T *__restrict
 // one side of a quantisation: int8 output, scale per tensor / input row / input column
 struct QSide {
   int8_t *q;  // NULL = side not wanted
-  int64_t ld;
+  int64_t ld;  // bytes per output row
   const double *scale;
   int gran, cap;
+  int packed = 0;  // row-major side only: two's-complement nibbles, column 2j in the low nibble of byte j
 };
 
 // quant_round (quant.py:70-71) in three fp64 instructions.  With scales from the true maxima
@@ -224,11 +225,20 @@ __global__ void __launch_bounds__(256) quantize_tile_kernel(const T *__restrict_
       if (GT) qt[j][k] = SAME ? qr[j][k] : qround<CLAMP>((double)v[j][k], GT == 1 ? st[j] : st[k], capt);
     }
   if (GR) {
-    int8_t *o = R.q + rb * R.ld + c;
+    if (R.packed) {  // four nibbles = 2 bytes per micro-tile row
+      int8_t *o = R.q + rb * R.ld + c / 2;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (interior || (rb + j < rows && c < R.ld))
-        *reinterpret_cast<uint32_t *>(o + j * R.ld) = pack4(qr[j][0], qr[j][1], qr[j][2], qr[j][3]);
+      for (int j = 0; j < 4; ++j)
+        if (interior || (rb + j < rows && c / 2 < R.ld))
+          *reinterpret_cast<uint16_t *>(o + j * R.ld) =
+              (uint16_t)((qr[j][0] & 0xF) | ((qr[j][1] & 0xF) << 4) | ((qr[j][2] & 0xF) << 8) | ((qr[j][3] & 0xF) << 12));
+    } else {
+      int8_t *o = R.q + rb * R.ld + c;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (interior || (rb + j < rows && c < R.ld))
+          *reinterpret_cast<uint32_t *>(o + j * R.ld) = pack4(qr[j][0], qr[j][1], qr[j][2], qr[j][3]);
+    }
   }
   if (GT) {
 #pragma unroll
@@ -394,6 +404,8 @@ int absmax_tile_launch(const T *x, int64_t rows, int64_t cols, int64_t ldx, doub
 
 // both sides' outputs must allow 4-byte stores (ld % 4, base alignment)
 bool tile_ok(const QSide &s) { return !s.q || (s.ld % 4 == 0 && (uintptr_t)s.q % 4 == 0); }
+// output columns a side spans (packed int4: two per byte)
+inline int64_t side_cols(const QSide &s) { return s.packed ? 2 * s.ld : s.ld; }
 
 inline int side_kind(const QSide &s) { return !s.q ? 0 : (s.gran == LRAMM_GRAN_ROW ? 1 : 2); }
 
@@ -408,7 +420,7 @@ void qtile_go(const T *x, int64_t rows, int64_t cols, int64_t ldx, const QSide &
 template <class T>
 int quantize_tile_launch(const T *x, int64_t rows, int64_t cols, int64_t ldx, const QSide &R, const QSide &Tq,
                          bool clamp, cudaStream_t st) {
-  const int64_t ext_r = std::max(rows, Tq.q ? Tq.ld : 0), ext_c = std::max(cols, R.q ? R.ld : 0);
+  const int64_t ext_r = std::max(rows, Tq.q ? Tq.ld : 0), ext_c = std::max(cols, R.q ? side_cols(R) : 0);
   const int64_t nbx = ceil_div(ext_c, 64), blocks = nbx * ceil_div(ext_r, 64);
   if (blocks >= (1LL << 31)) return fail(LRAMM_ERR_SHAPE, "quantize: %lld x %lld exceeds the tile grid",
                                          (long long)rows, (long long)cols);
@@ -537,7 +549,10 @@ int quantize_from_amax(const T *x, int64_t rows, int64_t cols, int64_t ldx, int 
   scales_from_amax_kernel<<<(unsigned)ceil_div(nscale, 256), 256, 0, st>>>(amax, nscale, cap, scales);
   LRAMM_LAUNCH_CHECK();
   const int64_t out_rows = transpose ? cols : rows;
-  if (q_dtype == LRAMM_I4) {
+  if (q_dtype == LRAMM_I4 && !transpose && ldq % 2 == 0 && (uintptr_t)q % 2 == 0 && x_vec_ok(x, ldx)) {
+    QSide side{(int8_t *)q, ldq, scales, gran, cap, 1}, none{nullptr, 0, nullptr, 0, 0};
+    return quantize_tile_launch<T>(x, rows, cols, ldx, side, none, clamp, st);
+  } else if (q_dtype == LRAMM_I4) {
     dim3 blk(32, 8);
     dim3 grid((unsigned)ceil_div(ldq, 32), (unsigned)ceil_div(out_rows, 8));
     quantize_int4_kernel<T><<<grid, blk, 0, st>>>(x, rows, cols, ldx, scales, gran, cap, transpose,
@@ -575,7 +590,7 @@ int quantize_impl(const T *x, int64_t rows, int64_t cols, int64_t ldx, int bits,
 template <class T>
 int quantize_pair_impl(const T *x, int64_t rows, int64_t cols, int64_t ldx, int bits_r, int gran_r, int8_t *qr,
                        int64_t ldqr, double *scales_r, int bits_t, int gran_t, int8_t *qt, int64_t ldqt,
-                       double *scales_t, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st) {
+                       double *scales_t, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st, int r_packed) {
   Arena ar(ws, ws_bytes);
   const bool need[3] = {gran_r == LRAMM_GRAN_TENSOR || gran_t == LRAMM_GRAN_TENSOR,
                         gran_r == LRAMM_GRAN_ROW || gran_t == LRAMM_GRAN_ROW,
@@ -595,9 +610,11 @@ int quantize_pair_impl(const T *x, int64_t rows, int64_t cols, int64_t ldx, int 
   LRAMM_LAUNCH_CHECK();
   scales_from_amax_kernel<<<(unsigned)ceil_div(n[gran_t], 256), 256, 0, st>>>(amax[gran_t], n[gran_t], cap_t, scales_t);
   LRAMM_LAUNCH_CHECK();
-  QSide R{qr, ldqr, scales_r, gran_r, cap_r}, Tq{qt, ldqt, scales_t, gran_t, cap_t};
-  if (tile_ok(R) && tile_ok(Tq) && x_vec_ok(x, ldx)) return quantize_tile_launch<T>(x, rows, cols, ldx, R, Tq, false, st);
-  LRAMM_TRY(quantize_from_amax<T>(x, rows, cols, ldx, bits_r, gran_r, 0, amax[gran_r], qr, LRAMM_I8, ldqr, scales_r, false, st));
+  QSide R{qr, ldqr, scales_r, gran_r, cap_r, r_packed}, Tq{qt, ldqt, scales_t, gran_t, cap_t};
+  const bool r_ok = r_packed ? (ldqr % 2 == 0 && (uintptr_t)qr % 2 == 0) : tile_ok(R);
+  if (r_ok && tile_ok(Tq) && x_vec_ok(x, ldx)) return quantize_tile_launch<T>(x, rows, cols, ldx, R, Tq, false, st);
+  LRAMM_TRY(quantize_from_amax<T>(x, rows, cols, ldx, bits_r, gran_r, 0, amax[gran_r], qr, r_packed ? LRAMM_I4 : LRAMM_I8,
+                                  ldqr, scales_r, false, st));
   return quantize_from_amax<T>(x, rows, cols, ldx, bits_t, gran_t, 1, amax[gran_t], qt, LRAMM_I8, ldqt, scales_t, false, st);
 }
 
@@ -652,18 +669,19 @@ int quantize_amax_device(const void *x, int x_dtype, int64_t rows, int64_t cols,
 // gran_t; gran in input coordinates) from a single absmax pass and a single read of x
 int quantize_pair_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits_r, int gran_r,
                          int8_t *qr, int64_t ldqr, double *scales_r, int bits_t, int gran_t, int8_t *qt, int64_t ldqt,
-                         double *scales_t, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st) {
+                         double *scales_t, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st, int r_packed) {
   if (rows < 1 || cols < 1 || ldx < cols) return fail(LRAMM_ERR_SHAPE, "quantize: bad shape");
   if (bits_r < 2 || bits_r > 8 || bits_t < 2 || bits_t > 8)
     return fail(LRAMM_ERR_UNSUPPORTED, "quantize pair: int8 outputs need bits in [2, 8]");
+  if (r_packed && bits_r > 4) return fail(LRAMM_ERR_UNSUPPORTED, "quantize pair: packed int4 needs bits <= 4");
   if (gran_r < 0 || gran_r > 2 || gran_t < 0 || gran_t > 2) return fail(LRAMM_ERR_PARAM, "bad granularity");
-  if (ldqr < cols || ldqt < rows) return fail(LRAMM_ERR_SHAPE, "quantize pair: ldq too small");
+  if ((r_packed ? 2 * ldqr : ldqr) < cols || ldqt < rows) return fail(LRAMM_ERR_SHAPE, "quantize pair: ldq too small");
   if (x_dtype == LRAMM_F32)
     return quantize_pair_impl<float>((const float *)x, rows, cols, ldx, bits_r, gran_r, qr, ldqr, scales_r, bits_t,
-                                     gran_t, qt, ldqt, scales_t, nonfinite, ws, ws_bytes, st);
+                                     gran_t, qt, ldqt, scales_t, nonfinite, ws, ws_bytes, st, r_packed);
   if (x_dtype == LRAMM_F64)
     return quantize_pair_impl<double>((const double *)x, rows, cols, ldx, bits_r, gran_r, qr, ldqr, scales_r, bits_t,
-                                      gran_t, qt, ldqt, scales_t, nonfinite, ws, ws_bytes, st);
+                                      gran_t, qt, ldqt, scales_t, nonfinite, ws, ws_bytes, st, r_packed);
   return fail(LRAMM_ERR_PARAM, "quantize: input dtype must be F32 or F64");
 }
 

@@ -216,6 +216,23 @@ def test_lramm_nonfinite_input_raises(L):
 # ------------------------------------------------------------------ L5 fast mode
 
 
+@pytest.mark.parametrize("shape", [(512, 384, 448), (300, 257, 199), (96, 33, 80)])
+@pytest.mark.parametrize("gran", ["tensor", "row"])
+def test_lramm_int4_sketch_vs_restatement(L, gran, shape):
+    # 4-bit sketch budget: X travels as packed int4 and is unpacked to int8 in shared memory by the
+    # GEMM (c3's Y = A . Omega); odd K exercises the half-filled last byte of each packed row
+    m, k, n = shape
+    a = O.synth(m, k, "exp:24", 9, 0, 0)
+    b = O.synth(k, n, "exp:24", 9, 0, 1)
+    kw = dict(rank=16, bits=(8, 8, 8), power_iters=1, oversample=6, seed=3)
+    ref = O.lramm(a, b, O.OracleParams(**kw, spec=O.SketchSpec(4, 8, 8, gran)))
+    d, _ = L.lramm(a, b, L.LrammParams(**kw, mode="fast", sketch_bits=4, power_bits=8, proj_bits=8, granularity=gran))
+    assert O.rel_fro(d, ref) <= 1e-3
+    f_ref = O.rsvd(a, 16, 1, 6, 7, O.SketchSpec(4, 4, 8, gran))  # power iteration at 4 bits too (packed X twice)
+    f = L.rsvd(a, L.RsvdParams(16, 1, 6, 7, mode="fast", sketch_bits=4, power_bits=4, proj_bits=8, granularity=gran))
+    assert np.max(np.abs(f.sigma - f_ref.sigma)) <= 1e-9 * f_ref.sigma[0]
+
+
 @pytest.mark.parametrize("gran", ["tensor", "row"])
 def test_lramm_fast_mode_vs_restatement(L, gran):
     a = O.synth(512, 512, "exp:24", 7, 0, 0)
