@@ -406,7 +406,7 @@ struct LrammBufs {
   int32_t *tmp32 = nullptr;  // int32 quantiser staging (bit budgets > 8)
   int64_t *acc64 = nullptr;  // exact int64 accumulator of multi-limb products
   int *nonfinite, *jinfo;
-  void *qws, *qws_b;  // quantiser scratch of the A-side / B-side streams
+  void *qws;
   size_t qbytes;
 };
 
@@ -447,7 +447,6 @@ LrammBufs carve_lramm(Arena &ar, int64_t m, int64_t k, int64_t n, int in_dtype, 
   int64_t mx = std::max(std::max(m, n), k);
   L.qbytes = quantize_ws_bytes(mx, mx);
   L.qws = ar.take<char>((int64_t)L.qbytes);
-  L.qws_b = ar.take<char>((int64_t)L.qbytes);
   return L;
 }
 
@@ -557,50 +556,33 @@ int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t 
   // ---- rsvd of both operands (pipeline.py:183-186): independent chains, so B runs on a
   // forked side stream (event fork/join; capturable into a CUDA graph)
   SideStream &side = side_stream(st);
-  if (b_ready) LRAMM_CUDA_TRY(cudaStreamWaitEvent(side.st, b_ready, 0));  // B (and C) uploaded on another stream
-  // The recombination operands that depend on one side only -- Vt = V_A^T, Usc = U_A sigma_A on A,
-  // W = U_B, Zsc^T = V_B sigma_B on B -- are scaled and quantised on that side's stream before the
-  // join (each qgemm quantises its operands independently, quant.py:110-113), so only E1 -> E2 -> E3
-  // and the quantisation of E1, E2 remain after it.  Multi-limb budgets (> 8 bits) share one int32
-  // staging buffer and keep the sequential order.
-  const bool early = L.vt.limbs <= 1 && L.wq.limbs <= 1 && L.zq.limbs <= 1 && L.uq.limbs <= 1 && !timings;
-  LRAMM_CUDA_TRY(cudaMemsetAsync(L.nonfinite, 0, 4 * sizeof(int), st));
-  LRAMM_CUDA_TRY(cudaEventRecord(side.fork, st));  // (nonfinite cleared before B's quantisers)
+  LRAMM_CUDA_TRY(cudaEventRecord(side.fork, st));
   LRAMM_CUDA_TRY(cudaStreamWaitEvent(side.st, side.fork, 0));
+  if (b_ready) LRAMM_CUDA_TRY(cudaStreamWaitEvent(side.st, b_ready, 0));  // B (and C) uploaded on another stream
   LRAMM_TRY(run_rsvd(b, in_dtype, L.rb, P, omega_b, L.UB, r, L.SB, L.VB, r, side.st));
-  auto side_b = [&](cudaStream_t sb, void *ws) -> int {
-    scale_cols_kernel<<<elem_grid(n * r), 256, 0, sb>>>(L.VB, n, (int)r, r, L.SB, L.Zsc, r);
-    LRAMM_LAUNCH_CHECK();
-    LRAMM_TRY(quant(L.UB, LRAMM_F64, k, r, r, d1, LRAMM_GRAN_TENSOR, 1, L.wq, L.nonfinite, ws, L.qbytes, sb, L.tmp32));
-    return quant(L.Zsc, LRAMM_F64, n, r, r, d2, LRAMM_GRAN_TENSOR, 0, L.zq, L.nonfinite, ws, L.qbytes, sb, L.tmp32);
-  };
-  auto side_a = [&](cudaStream_t sa) -> int {
-    scale_cols_kernel<<<elem_grid(m * r), 256, 0, sa>>>(L.UA, m, (int)r, r, L.SA, L.Usc, r);
-    LRAMM_LAUNCH_CHECK();
-    LRAMM_TRY(quant(L.VA, LRAMM_F64, k, r, r, d1, LRAMM_GRAN_TENSOR, 1, L.vt, L.nonfinite, L.qws, L.qbytes, sa, L.tmp32));
-    return quant(L.Usc, LRAMM_F64, m, r, r, d3, LRAMM_GRAN_TENSOR, 0, L.uq, L.nonfinite, L.qws, L.qbytes, sa, L.tmp32);
-  };
-  if (early) LRAMM_TRY(side_b(side.st, L.qws_b));
   LRAMM_TRY(run_rsvd(a, in_dtype, L.ra, P, omega_a, L.UA, r, L.SA, L.VA, r, st));
-  if (early) LRAMM_TRY(side_a(st));
   LRAMM_CUDA_TRY(cudaEventRecord(side.join, side.st));
   LRAMM_CUDA_TRY(cudaStreamWaitEvent(st, side.join, 0));
   LRAMM_TRY(mark(1));
-  // ---- scaling (pipeline.py:188-193): Usc = U_A sigma_A, Zsc^T = V_B sigma_B; E1's, E2's and E3's
-  // single-side operands (quant.py:110-113)
-  if (!early) {
-    LRAMM_TRY(side_a(st));
-    LRAMM_TRY(side_b(st, L.qws));
-  }
+  // ---- scaling (pipeline.py:188-193): Usc = U_A sigma_A, Zsc^T = V_B sigma_B
+  scale_cols_kernel<<<elem_grid(m * r), 256, 0, st>>>(L.UA, m, (int)r, r, L.SA, L.Usc, r);
+  LRAMM_LAUNCH_CHECK();
+  scale_cols_kernel<<<elem_grid(n * r), 256, 0, st>>>(L.VB, n, (int)r, r, L.SB, L.Zsc, r);
+  LRAMM_LAUNCH_CHECK();
   LRAMM_TRY(mark(2));
+  LRAMM_CUDA_TRY(cudaMemsetAsync(L.nonfinite, 0, 4 * sizeof(int), st));
   // ---- E1 = QM(V_A^T U_B, d1)   (r x r, K = k)
+  LRAMM_TRY(quant(L.VA, LRAMM_F64, k, r, r, d1, LRAMM_GRAN_TENSOR, 1, L.vt, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
+  LRAMM_TRY(quant(L.UB, LRAMM_F64, k, r, r, d1, LRAMM_GRAN_TENSOR, 1, L.wq, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
   LRAMM_TRY(qprod(L.vt, L.wq, r, r, k, L.E1, r, 0, L.e1acc, st, L.acc64));
   LRAMM_TRY(mark(3));
   // ---- E2 = QM(E1 Zsc, d2)   (r x n, K = r) stored transposed for E3
   LRAMM_TRY(quant(L.E1, LRAMM_F64, r, r, r, d2, LRAMM_GRAN_TENSOR, 0, L.e1q, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
+  LRAMM_TRY(quant(L.Zsc, LRAMM_F64, n, r, r, d2, LRAMM_GRAN_TENSOR, 0, L.zq, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
   LRAMM_TRY(qprod(L.e1q, L.zq, r, n, r, L.E2T, r, 1, nullptr, st, L.acc64));
   LRAMM_TRY(mark(4));
   // ---- E3 = QM(Usc E2, d3) ; D = alpha E3 + beta C   (m x n, K = r)
+  LRAMM_TRY(quant(L.Usc, LRAMM_F64, m, r, r, d3, LRAMM_GRAN_TENSOR, 0, L.uq, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
   LRAMM_TRY(quant(L.E2T, LRAMM_F64, n, r, r, d3, LRAMM_GRAN_TENSOR, 0, L.e2q, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
   {
     lramm_epilogue_t e = {};
