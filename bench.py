@@ -435,7 +435,11 @@ def run_ours(args, cfg, world, rank, local):
             "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches, "roofline": roof,
             "stages": stages}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in CPU_SAMPLE_CONFIGS:
-        line["cpu_baseline"] = cpu_baseline(cfg, a, b)
+        line["cpu_baseline"], d_ref = cpu_baseline(cfg, a, b)
+    else:
+        d_ref = None
+    if rank == 0:
+        line["accuracy"] = accuracy(L, cfg, a, b, outs[0], d_ref)
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
@@ -657,11 +661,37 @@ def cpu_baseline(cfg, a, b):
     params = ref.LrammParams(rank=cfg["rank"], bits=tuple(cfg["bits"]), power_iters=cfg["power_iters"],
                              oversample=cfg["oversample"], seed=0)
     t0 = time.perf_counter()
-    ref.lramm(ha, hb, params)
+    d_ref, _ = ref.lramm(ha, hb, params)
     t = time.perf_counter() - t0
     return {"value": effective_ops(cfg) / t / 1e12, "unit": "TOPS", "cores": os.cpu_count(), "kind": "reference",
             "sample": f"one full reference lramm() call on the same {cfg['m']}x{cfg['k']}x{cfg['n']} inputs "
-                      f"({t:.1f} s, backend {ref.backend_name()}, OpenBLAS threads = host cores)"}
+                      f"({t:.1f} s, backend {ref.backend_name()}, OpenBLAS threads = host cores)"}, d_ref
+
+
+def accuracy(L, cfg, a, b, d_ours, d_ref=None):
+    """Report only, after the timed region: relative Frobenius error of the benchmarked (fast-mode)
+    product against the exact fp64 product, next to the reference's own error on the same inputs,
+    and -- where the reference ran -- this package's parity-mode product (the reference's algorithm:
+    fp64 sketches, per-tensor QM) against the reference's output (the <= 1e-3 gate)."""
+    import torch
+
+    exact = a.double() @ b.double()
+    nrm = torch.linalg.norm(exact)
+    out = {"rel_err_vs_exact": float(torch.linalg.norm(d_ours.double() - exact) / nrm),
+           "exact": "fp64 product of the same fp32 inputs"}
+    if d_ref is not None:
+        dr = torch.from_numpy(np.ascontiguousarray(d_ref)).to(exact.device)
+        e_ref = float(torch.linalg.norm(dr - exact) / nrm)
+        out["reference_rel_err_vs_exact"] = e_ref
+        out["fast_mode_error_within_2pct_of_reference"] = abs(out["rel_err_vs_exact"] - e_ref) <= 0.02 * e_ref
+        p = L.LrammParams(rank=cfg["rank"], bits=tuple(cfg["bits"]), power_iters=cfg["power_iters"],
+                          oversample=cfg["oversample"], seed=0)  # parity mode: the reference's algorithm
+        d_par, _, _ = L.lramm_device(a, b, p)
+        out["parity_mode_rel_diff_vs_reference"] = float(torch.linalg.norm(d_par.double() - dr) / torch.linalg.norm(dr))
+        out["note"] = ("fast mode (int8 sketches, the benchmarked path) has no reference counterpart: its gate is "
+                       "accuracy parity; the parity-mode output is gated at <= 1e-3 relative Frobenius vs the "
+                       "reference's output")
+    return out
 
 
 if __name__ == "__main__":
