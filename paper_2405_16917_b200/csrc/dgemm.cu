@@ -8,6 +8,7 @@
 // buffered shared memory with cp.async.  trans_a = 1 evaluates A^T.B for tall
 // row-major operands (A: K x M) with split-K over the long dimension and a
 // fixed-order reduction, so results are bitwise reproducible run to run.
+#include <cstdlib>
 #include <algorithm>
 #include <mutex>
 
@@ -225,6 +226,8 @@ int64_t tile_count(int64_t M, int64_t N, bool sym) {
 }
 
 int choose_splits(int trans_a, int64_t M, int64_t N, int64_t K, bool sym = false) {
+  static const int env = getenv("LRAMM_DGEMM_SPLIT") ? atoi(getenv("LRAMM_DGEMM_SPLIT")) : 0;
+  if (env > 0) return (int)std::min<int64_t>(std::min(env, 64), std::max<int64_t>(1, K / 16));
   int64_t tiles = tile_count(M, N, sym);
   // ~4 waves of 4 resident CTAs per SM when K is long enough (wave quantisation stays small);
   // each split keeps >= 256 of K (max_by_k)
