@@ -130,6 +130,9 @@ struct QSide {
   const double *scale;
   int gran, cap;
   int packed = 0;  // row-major side only: two's-complement nibbles, column 2j in the low nibble of byte j
+  // non-NULL: the kernel derives the scales from these maxima itself (quant_scale) and writes
+  // them to `scale` (no separate scales kernel)
+  const double *amax = nullptr;
 };
 
 // quant_round (quant.py:70-71) in three fp64 instructions.  With scales from the true maxima
@@ -175,8 +178,37 @@ __device__ __forceinline__ void side_scales(const QSide &s, int64_t rb, int64_t 
                                             double (&sc)[4]) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    if (G == 1) sc[i] = rb + i < rows ? s.scale[rb + i] : 0.0;
-    else if (G == 2) sc[i] = s.gran == LRAMM_GRAN_TENSOR ? s.scale[0] : (c + i < cols ? s.scale[c + i] : 0.0);
+    if (s.amax) {  // scales derived here from the maxima (published by publish_scales)
+      if (G == 1) sc[i] = rb + i < rows ? quant_scale(s.amax[rb + i], s.cap) : 0.0;
+      else if (G == 2)
+        sc[i] = s.gran == LRAMM_GRAN_TENSOR ? quant_scale(s.amax[0], s.cap)
+                                            : (c + i < cols ? quant_scale(s.amax[c + i], s.cap) : 0.0);
+    } else {
+      if (G == 1) sc[i] = rb + i < rows ? s.scale[rb + i] : 0.0;
+      else if (G == 2) sc[i] = s.gran == LRAMM_GRAN_TENSOR ? s.scale[0] : (c + i < cols ? s.scale[c + i] : 0.0);
+    }
+  }
+}
+
+// With QSide::amax the kernel writes the scales it derived: row scales by the first tile column
+// (c0 == 0, one thread per micro-tile row), column scales by the first tile row, the tensor
+// scale by thread 0 of block 0.
+template <int G>
+__device__ __forceinline__ void publish_scales(const QSide &s, int64_t rb, int64_t c, int64_t rows, int64_t cols,
+                                               const double (&sc)[4]) {
+  if (!s.amax) return;
+  double *out = const_cast<double *>(s.scale);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (G == 1) {
+      if (rb + i < rows && (threadIdx.x & 15) == 0 && c < 64) out[rb + i] = sc[i];
+    } else if (G == 2) {
+      if (s.gran == LRAMM_GRAN_TENSOR) {
+        if (i == 0 && blockIdx.x == 0 && threadIdx.x == 0) out[0] = sc[0];
+      } else if (c + i < cols && (threadIdx.x >> 4) == 0 && rb < 64) {
+        out[c + i] = sc[i];
+      }
+    }
   }
 }
 
@@ -215,6 +247,8 @@ __global__ void __launch_bounds__(256) quantize_tile_kernel(const T *__restrict_
   double sr[4], st[4];
   if (GR) side_scales<GR>(R, rb, c, rows, cols, sr);
   if (GT && !SAME) side_scales<GT>(Tq, rb, c, rows, cols, st);
+  if (GR) publish_scales<GR>(R, rb, c, rows, cols, sr);
+  if (GT) publish_scales<GT>(Tq, rb, c, rows, cols, SAME ? sr : st);
   const double capr = (double)R.cap, capt = (double)Tq.cap;
   uint32_t qr[4][4], qt[4][4];
 #pragma unroll
@@ -546,20 +580,23 @@ int quantize_from_amax(const T *x, int64_t rows, int64_t cols, int64_t ldx, int 
                        cudaStream_t st) {
   const int cap = bit_cap(bits);
   const int64_t nscale = gran == LRAMM_GRAN_TENSOR ? 1 : (gran == LRAMM_GRAN_ROW ? rows : cols);
+  const int64_t out_rows = transpose ? cols : rows;
+  // the tile kernel derives and publishes the scales itself
+  if (q_dtype == LRAMM_I4 && !transpose && ldq % 2 == 0 && (uintptr_t)q % 2 == 0 && x_vec_ok(x, ldx)) {
+    QSide side{(int8_t *)q, ldq, scales, gran, cap, 1, amax}, none{nullptr, 0, nullptr, 0, 0};
+    return quantize_tile_launch<T>(x, rows, cols, ldx, side, none, clamp, st);
+  }
+  if (q_dtype == LRAMM_I8 && tile_ok(QSide{(int8_t *)q, ldq, scales, gran, cap}) && x_vec_ok(x, ldx)) {
+    QSide side{(int8_t *)q, ldq, scales, gran, cap, 0, amax}, none{nullptr, 0, nullptr, 0, 0};
+    return quantize_tile_launch<T>(x, rows, cols, ldx, transpose ? none : side, transpose ? side : none, clamp, st);
+  }
   scales_from_amax_kernel<<<(unsigned)ceil_div(nscale, 256), 256, 0, st>>>(amax, nscale, cap, scales);
   LRAMM_LAUNCH_CHECK();
-  const int64_t out_rows = transpose ? cols : rows;
-  if (q_dtype == LRAMM_I4 && !transpose && ldq % 2 == 0 && (uintptr_t)q % 2 == 0 && x_vec_ok(x, ldx)) {
-    QSide side{(int8_t *)q, ldq, scales, gran, cap, 1}, none{nullptr, 0, nullptr, 0, 0};
-    return quantize_tile_launch<T>(x, rows, cols, ldx, side, none, clamp, st);
-  } else if (q_dtype == LRAMM_I4) {
+  if (q_dtype == LRAMM_I4) {
     dim3 blk(32, 8);
     dim3 grid((unsigned)ceil_div(ldq, 32), (unsigned)ceil_div(out_rows, 8));
     quantize_int4_kernel<T><<<grid, blk, 0, st>>>(x, rows, cols, ldx, scales, gran, cap, transpose,
                                                   (uint8_t *)q, ldq);
-  } else if (q_dtype == LRAMM_I8 && tile_ok(QSide{(int8_t *)q, ldq, scales, gran, cap}) && x_vec_ok(x, ldx)) {
-    QSide side{(int8_t *)q, ldq, scales, gran, cap}, none{nullptr, 0, nullptr, 0, 0};
-    return quantize_tile_launch<T>(x, rows, cols, ldx, transpose ? none : side, transpose ? side : none, clamp, st);
   } else {
     dim3 blk(32, 8);
     dim3 grid((unsigned)ceil_div(ldq, kTile), (unsigned)ceil_div(out_rows, kTile));
@@ -606,13 +643,13 @@ int quantize_pair_impl(const T *x, int64_t rows, int64_t cols, int64_t ldx, int 
   LRAMM_CUDA_TRY(cudaMemsetAsync(base, 0, total * sizeof(double), st));
   LRAMM_TRY(absmax_tile_launch<T>(x, rows, cols, ldx, amax[0], amax[1], amax[2], nonfinite, st));
   const int cap_r = bit_cap(bits_r), cap_t = bit_cap(bits_t);
+  QSide R{qr, ldqr, scales_r, gran_r, cap_r, r_packed, amax[gran_r]}, Tq{qt, ldqt, scales_t, gran_t, cap_t, 0, amax[gran_t]};
+  const bool r_ok = r_packed ? (ldqr % 2 == 0 && (uintptr_t)qr % 2 == 0) : tile_ok(R);
+  if (r_ok && tile_ok(Tq) && x_vec_ok(x, ldx)) return quantize_tile_launch<T>(x, rows, cols, ldx, R, Tq, false, st);
   scales_from_amax_kernel<<<(unsigned)ceil_div(n[gran_r], 256), 256, 0, st>>>(amax[gran_r], n[gran_r], cap_r, scales_r);
   LRAMM_LAUNCH_CHECK();
   scales_from_amax_kernel<<<(unsigned)ceil_div(n[gran_t], 256), 256, 0, st>>>(amax[gran_t], n[gran_t], cap_t, scales_t);
   LRAMM_LAUNCH_CHECK();
-  QSide R{qr, ldqr, scales_r, gran_r, cap_r, r_packed}, Tq{qt, ldqt, scales_t, gran_t, cap_t};
-  const bool r_ok = r_packed ? (ldqr % 2 == 0 && (uintptr_t)qr % 2 == 0) : tile_ok(R);
-  if (r_ok && tile_ok(Tq) && x_vec_ok(x, ldx)) return quantize_tile_launch<T>(x, rows, cols, ldx, R, Tq, false, st);
   LRAMM_TRY(quantize_from_amax<T>(x, rows, cols, ldx, bits_r, gran_r, 0, amax[gran_r], qr, r_packed ? LRAMM_I4 : LRAMM_I8,
                                   ldqr, scales_r, false, st));
   return quantize_from_amax<T>(x, rows, cols, ldx, bits_t, gran_t, 1, amax[gran_t], qt, LRAMM_I8, ldqt, scales_t, false, st);
