@@ -168,6 +168,12 @@ int lramm_scale_round_clip(const double *a, int64_t rows, int64_t cols, int64_t 
  * int32 output with accumulate = 1. */
 int lramm_igemm(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, const int8_t *b,
                 int64_t ldb, const lramm_epilogue_t *epi, int split_k, lramm_stream_t stream);
+/* The same product with A packed int4 (two's-complement nibbles, column 2j in the low nibble of
+ * byte j, lda in bytes, a multiple of 16 and >= ceil(K/2)), as lramm_quantize writes it for
+ * q_dtype = LRAMM_I4 (bit budgets <= 4).  tcgen05 has no int4 kind on sm_100: the kernel
+ * unpacks the TMA-loaded tile to int8 in shared memory before kind::i8 (c3's Y = A . Omega). */
+int lramm_igemm_i4(int64_t M, int64_t N, int64_t K, const uint8_t *a4, int64_t lda, const int8_t *b,
+                   int64_t ldb, const lramm_epilogue_t *epi, int split_k, lramm_stream_t stream);
 
 /* Bit budgets 9..24 (quant.py:16-28 allows [2, 24]): a quantised int32 operand is carried as
  * 1..4 planes of 8-bit limbs, v = sum_l limb_l 256^l (unsigned low limbs, signed top limb).

@@ -91,6 +91,7 @@ SIGNATURES = {
     "lramm_cholqr_pass_ws": (_sz, [_i64, _i64]),
     "lramm_dequant": (_i32, [_vp, _i64, _i64, _i64, _P(Epilogue), _vp]),
     "lramm_igemm": (_i32, [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _P(Epilogue), _i32, _vp]),
+    "lramm_igemm_i4": (_i32, [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _P(Epilogue), _i32, _vp]),
     "lramm_omega": (_i32, [ctypes.c_uint64, ctypes.c_uint64, _i64, _i64, _vp, _vp, _sz, _vp]),
     "lramm_omega_ws": (_sz, [_i64, _i64]),
     "lramm_split_limbs": (_i32, [_vp, _i64, _i64, _i64, _i32, _vp, _i64, _vp]),

@@ -221,6 +221,12 @@ int lramm_igemm(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, c
   return igemm_device(M, N, K, a, lda, b, ldb, *epi, split_k, (cudaStream_t)stream);
 }
 
+int lramm_igemm_i4(int64_t M, int64_t N, int64_t K, const uint8_t *a4, int64_t lda, const int8_t *b, int64_t ldb,
+                   const lramm_epilogue_t *epi, int split_k, lramm_stream_t stream) {
+  if (!epi) return fail(LRAMM_ERR_PARAM, "igemm_i4: epilogue is NULL");
+  return igemm_device(M, N, K, (const int8_t *)a4, lda, b, ldb, *epi, split_k, (cudaStream_t)stream, 1);
+}
+
 int lramm_omega(uint64_t key0, uint64_t key1, int64_t ncols, int64_t w, double *out, void *ws, size_t ws_bytes,
                 lramm_stream_t stream) {
   return omega_device(key0, key1, ncols, w, out, ws, ws_bytes, (cudaStream_t)stream);

@@ -7,6 +7,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <mutex>
 #include <string>
 
 #include "../../include/lramm_cuda.h"
@@ -64,6 +65,24 @@ inline cudaError_t allow_max_dyn_smem(K kernel) {
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
 }
+
+// Run a setup step (kernel attributes, symbol uploads) once per device: function attributes
+// such as the dynamic shared-memory limit are per device, so a process-wide call_once would
+// leave the second device of a multi-GPU process with the default limit.
+struct PerDeviceOnce {
+  static constexpr int kMaxDev = 64;
+  std::once_flag flags[kMaxDev];
+  cudaError_t err[kMaxDev] = {};
+  template <class F>
+  cudaError_t run(F &&f) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDev) return f();
+    std::call_once(flags[dev], [&] { err[dev] = f(); });
+    return err[dev];
+  }
+};
 
 // Bump allocator over a caller-provided workspace (256-byte aligned slices).
 struct Arena {

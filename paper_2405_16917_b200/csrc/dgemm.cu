@@ -226,8 +226,6 @@ int64_t tile_count(int64_t M, int64_t N, bool sym) {
 }
 
 int choose_splits(int trans_a, int64_t M, int64_t N, int64_t K, bool sym = false) {
-  static const int env = getenv("LRAMM_DGEMM_SPLIT") ? atoi(getenv("LRAMM_DGEMM_SPLIT")) : 0;
-  if (env > 0) return (int)std::min<int64_t>(std::min(env, 64), std::max<int64_t>(1, K / 16));
   int64_t tiles = tile_count(M, N, sym);
   // ~4 waves of 4 resident CTAs per SM when K is long enough (wave quantisation stays small);
   // each split keeps >= 256 of K (max_by_k)
@@ -259,14 +257,14 @@ int dgemm_device_ex(int trans_a, int64_t M, int64_t N, int64_t K, const double *
                   : dim3((unsigned)ceil_div(M, TM), (unsigned)ceil_div(N, TN), (unsigned)splits);
   double *out = splits > 1 ? (double *)ws : C;
   int64_t ldo = splits > 1 ? N : ldc;
-  static std::once_flag once;
-  static cudaError_t e = cudaSuccess;
-  std::call_once(once, [&] {
+  static PerDeviceOnce once;
+  LRAMM_CUDA_TRY(once.run([] {
+    cudaError_t e = cudaSuccess;
     for (auto k : {dgemm_kernel<true, true>, dgemm_kernel<true, false>, dgemm_kernel<false, true>,
                    dgemm_kernel<false, false>})
       if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDgemmSmem);
-  });
-  LRAMM_CUDA_TRY(e);
+    return e;
+  }));
   const int direct = splits == 1;
   const bool vec = ((lda | ldb) % 2 == 0) && (((uintptr_t)A | (uintptr_t)B) % 16 == 0);
   auto kern = trans_a ? (vec ? dgemm_kernel<true, true> : dgemm_kernel<true, false>)

@@ -180,7 +180,7 @@ RsvdBufs carve_rsvd(Arena &ar, int64_t rows, int64_t cols, int x_dtype, const lr
 
 // C (M x N fp64) = dequant(A . B^T): row scales of A, column scales of B
 int qprod(const QOp &A, const QOp &B, int64_t M, int64_t N, int64_t K, double *C, int64_t ldc, int transpose_out,
-          int32_t *acc, cudaStream_t st, int64_t *acc64 = nullptr) {
+          int32_t *acc, cudaStream_t st, int64_t *acc64 = nullptr, bool force64 = false) {
   lramm_epilogue_t e = {};
   e.out_dtype = LRAMM_F64;
   e.transpose_out = transpose_out;
@@ -192,7 +192,7 @@ int qprod(const QOp &A, const QOp &B, int64_t M, int64_t N, int64_t K, double *C
   e.col_scale_inc = B.inc;
   e.alpha = 1.0;
   e.beta = 0.0;
-  if (A.limbs > 1 || B.limbs > 1) {
+  if (A.limbs > 1 || B.limbs > 1 || force64) {
     if (!acc64) return fail(LRAMM_ERR_WORKSPACE, "qprod: multi-limb product needs an int64 accumulator");
     return igemm_limbs_device(M, N, K, A.q, A.ld, A.plane, A.limbs, B.q, B.ld, B.plane, B.limbs, acc64, e, st);
   }
@@ -202,8 +202,6 @@ int qprod(const QOp &A, const QOp &B, int64_t M, int64_t N, int64_t K, double *C
   // split-K into at most one wave of CTAs (4096 x 272 x 4096 sketch: 64 tiles -> split 2, 4.15 -> 4.07 ms
   // c2 step against split 3's 1.3 waves)
   if (acc && tiles * 2 <= num_sms() && kb >= 8) split = (int)std::min<int64_t>(kb / 4, num_sms() / tiles);
-  static const int split_env = getenv("LRAMM_QPROD_SPLIT") ? atoi(getenv("LRAMM_QPROD_SPLIT")) : 0;
-  if (split_env > 0 && acc) split = (int)std::min<int64_t>(split_env, kb);
   if (split <= 1) return igemm_device(M, N, K, A.q, A.ld, B.q, B.ld, e, 1, st, A.packed);
   LRAMM_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)M * N * sizeof(int32_t), st));
   lramm_epilogue_t ea = {};
@@ -235,14 +233,17 @@ int check_bits_dev(int bits, const char *what, bool limbs_ok = false) {
   return LRAMM_OK;
 }
 
-// recombination guard: the reference's int64 rule (quant.py:87-93) for multi-limb products (their
-// int64 accumulation is exact), the int32 rule for single int8 products
-int check_acc(int64_t K, int bits_a, int bits_b);
+// recombination guard: the reference's int64 rule (quant.py:87-93) is the only refusal; products
+// whose int32 accumulators could overflow (K cap^2 >= 2^31) run through the exact int64 limb
+// path (igemm_limbs_device: K chunked so every int32 partial is exact)
 int check_acc_qm(int64_t K, int bits) {
-  if (bits <= 8) return check_acc(K, bits, bits);
   if ((long double)K * bit_cap(bits) * bit_cap(bits) >= 9223372036854775808.0L)
     return fail(LRAMM_ERR_OVERFLOW, "k=%lld with bit budgets (%d, %d) risks int64 overflow", (long long)K, bits, bits);
   return LRAMM_OK;
+}
+// does a single-int8 product of contraction length K need the int64 accumulator?
+bool needs_acc64(int64_t K, int bits) {
+  return bits <= 8 && (double)K * bit_cap(bits) * bit_cap(bits) >= 2147483648.0;
 }
 
 // int32 accumulation guard: K * cap_a * cap_b < 2^31 (the reference's int64 guard is quant.py:87-93)
@@ -435,11 +436,13 @@ LrammBufs carve_lramm(Arena &ar, int64_t m, int64_t k, int64_t n, int in_dtype, 
   if (l1 > 1 || l2 > 1 || l3 > 1) {
     const int64_t mx = std::max(std::max(m, n), k);
     L.tmp32 = ar.take<int32_t>(mx * round_up(std::max(k, r), 16));
+  }
+  {
     int64_t acc_elems = 0;
-    if (l1 > 1) acc_elems = std::max(acc_elems, r * r);
-    if (l2 > 1) acc_elems = std::max(acc_elems, r * n);
-    if (l3 > 1) acc_elems = std::max(acc_elems, m * n);
-    L.acc64 = ar.take<int64_t>(acc_elems);
+    if (l1 > 1 || needs_acc64(k, P.bits[0])) acc_elems = std::max(acc_elems, r * r);
+    if (l2 > 1 || needs_acc64(r, P.bits[1])) acc_elems = std::max(acc_elems, r * n);
+    if (l3 > 1 || needs_acc64(r, P.bits[2])) acc_elems = std::max(acc_elems, m * n);
+    if (acc_elems) L.acc64 = ar.take<int64_t>(acc_elems);
   }
   L.e1acc = ar.take<int32_t>(r * r);
   L.nonfinite = ar.take<int>(4);
@@ -574,12 +577,12 @@ int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t 
   // ---- E1 = QM(V_A^T U_B, d1)   (r x r, K = k)
   LRAMM_TRY(quant(L.VA, LRAMM_F64, k, r, r, d1, LRAMM_GRAN_TENSOR, 1, L.vt, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
   LRAMM_TRY(quant(L.UB, LRAMM_F64, k, r, r, d1, LRAMM_GRAN_TENSOR, 1, L.wq, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
-  LRAMM_TRY(qprod(L.vt, L.wq, r, r, k, L.E1, r, 0, L.e1acc, st, L.acc64));
+  LRAMM_TRY(qprod(L.vt, L.wq, r, r, k, L.E1, r, 0, L.e1acc, st, L.acc64, needs_acc64(k, d1)));
   LRAMM_TRY(mark(3));
   // ---- E2 = QM(E1 Zsc, d2)   (r x n, K = r) stored transposed for E3
   LRAMM_TRY(quant(L.E1, LRAMM_F64, r, r, r, d2, LRAMM_GRAN_TENSOR, 0, L.e1q, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
   LRAMM_TRY(quant(L.Zsc, LRAMM_F64, n, r, r, d2, LRAMM_GRAN_TENSOR, 0, L.zq, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
-  LRAMM_TRY(qprod(L.e1q, L.zq, r, n, r, L.E2T, r, 1, nullptr, st, L.acc64));
+  LRAMM_TRY(qprod(L.e1q, L.zq, r, n, r, L.E2T, r, 1, nullptr, st, L.acc64, needs_acc64(r, d2)));
   LRAMM_TRY(mark(4));
   // ---- E3 = QM(Usc E2, d3) ; D = alpha E3 + beta C   (m x n, K = r)
   LRAMM_TRY(quant(L.Usc, LRAMM_F64, m, r, r, d3, LRAMM_GRAN_TENSOR, 0, L.uq, L.nonfinite, L.qws, L.qbytes, st, L.tmp32));
@@ -598,7 +601,7 @@ int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t 
     e.c = c;
     e.c_dtype = c_dtype;
     e.ldc = n;
-    if (L.uq.limbs > 1)
+    if (L.uq.limbs > 1 || needs_acc64(r, d3))
       LRAMM_TRY(igemm_limbs_device(m, n, r, L.uq.q, L.uq.ld, L.uq.plane, L.uq.limbs, L.e2q.q, L.e2q.ld, L.e2q.plane,
                                    L.e2q.limbs, L.acc64, e, st));
     else

@@ -413,11 +413,7 @@ int absmax_tile_launch(const T *x, int64_t rows, int64_t cols, int64_t ldx, doub
   const int64_t nbx = ceil_div(cols, 64LL * V), blocks = nbx * ceil_div(rows, 64);
   if (ceil_div(cols, 64) * ceil_div(rows, 64) >= (1LL << 31))
     return fail(LRAMM_ERR_SHAPE, "absmax: %lld x %lld exceeds the tile grid", (long long)rows, (long long)cols);
-  static const int micro_env = [] {
-    const char *e = getenv("LRAMM_ABSMAX_MICRO");
-    return e ? atoi(e) : -1;
-  }();
-  const bool micro = x_vec_ok(x, ldx) && (micro_env >= 0 ? micro_env == 1 : sizeof(T) == 8);
+  const bool micro = x_vec_ok(x, ldx) && sizeof(T) == 8;
   if (micro) {
     switch (mask) {
       case 1: absmax_micro_go<T, 1>(x, rows, cols, ldx, amax_t, amax_r, amax_c, nonfinite, st); break;

@@ -202,8 +202,8 @@ def lramm_device(a: torch.Tensor, b: torch.Tensor, params: LrammParams, c: torch
     wb = sketch_width((k, n), params.rank, params.oversample)
     om_a = OMEGA.device_omega(seed_a, k, wa, dev)
     om_b = OMEGA.device_omega(seed_b, n, wb, dev)
-    if a.dtype != b.dtype:
-        b = b.to(a.dtype)
+    if a.dtype != b.dtype:  # mixed fp32 / fp64: both in float64, like as_matrix (matcore.py:31-38)
+        a, b = a.to(torch.float64), b.to(torch.float64)
     p = _params(params)
     out_t = torch.float64 if np.dtype(params.out_dtype) == np.float64 else torch.float32
     if out is None:

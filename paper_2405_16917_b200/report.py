@@ -21,7 +21,6 @@ from .pipeline import CostModel, LrammParams, gemm, lramm
 from .quant import bit_cap, dequantize, quantize
 from .rsvd import RsvdParams, oracle_svd, rsvd, truncate_svd
 
-ORACLE_MAX_MIN_DIM = 512  # matcore.py:23: above this the reference estimates sigmas by rsvd
 
 
 # ------------------------------------------------------------------ bounds (bounds.py)
@@ -185,7 +184,9 @@ def leading_sigmas(a, count, seed=0):
     shape = _shape(a)
     if len(shape) != 2:
         raise ShapeError("matrix must be 2-D")
-    if min(shape) <= ORACLE_MAX_MIN_DIM:
+    from . import rsvd as _rsvd  # the oracle cap (matcore.py:23), read at call time
+
+    if min(shape) <= _rsvd.ORACLE_MAX_MIN_DIM:
         return np.asarray(oracle_svd(a).sigma)[:count], "oracle"
     f = rsvd(a, RsvdParams(rank=min(count, min(shape)), power_iters=1, seed=seed))
     return np.asarray(f.sigma)[:count], "rsvd"
@@ -241,7 +242,11 @@ def evaluate(a, b, params: LrammParams, c=None):
     ee = ee.to(dd.device, torch.float64)
     fro = _fro(dd.to(torch.float64) - ee)
     denom = _fro(ee)
-    rel = fro / denom if denom > 0 else (0.0 if fro == 0 else math.inf)
+    if denom == 0.0:  # matcore.relative_error (matcore.py:196-198), called by evaluate (pipeline.py:308)
+        from .errors import DegenerateDenominatorError
+
+        raise DegenerateDenominatorError("exact matrix has zero Frobenius norm")
+    rel = fro / denom
     bound, source = combined_bound(a, b, params)
     d1, d2, d3 = params.bits
     m, k = _shape(a)

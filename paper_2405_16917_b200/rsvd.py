@@ -196,11 +196,21 @@ def truncate_svd(factors, rank):
                       v=np.ascontiguousarray(factors.v[:, :rank]))
 
 
+# Size cap of the dense SVD oracle (matcore.py:20-23), read at call time like the reference's
+# module constant, so a harness may raise it.
+ORACLE_MAX_MIN_DIM = 512
+
+
 def oracle_svd(a):
-    """Dense SVD (matcore.py:232-245) on device: CholeskyQR2 + one-sided Jacobi, no size cap."""
+    """Dense SVD (matcore.py:232-245) on device: CholeskyQR2 + one-sided Jacobi, capped at
+    min(m, n) <= ORACLE_MAX_MIN_DIM (OracleLimitError above it, matcore.py:240-243)."""
     from . import kernels
+    from .errors import OracleLimitError
 
     if isinstance(a, torch.Tensor):
         a = a.detach().cpu().numpy()
+    a = np.asarray(a)
+    if a.ndim == 2 and min(a.shape) > ORACLE_MAX_MIN_DIM:
+        raise OracleLimitError(f"oracle SVD capped at min dim {ORACLE_MAX_MIN_DIM}, got {a.shape}")
     u, s, v = kernels.svd(np.ascontiguousarray(a, dtype=np.float64))
     return SvdFactors(u=u, sigma=s, v=v)

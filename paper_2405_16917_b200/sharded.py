@@ -28,7 +28,9 @@ import torch
 
 from . import _native as N
 from ._device import OMEGA, WORKSPACE, ptr, stream_handle
+from .errors import OverflowRiskError, UnsupportedError
 from .pipeline import _child_seeds
+from .quant import bit_cap
 from .rsvd import sketch_width
 
 GRAN = {"tensor": N.GRAN_TENSOR, "row": N.GRAN_ROW, "col": N.GRAN_COL}
@@ -192,6 +194,16 @@ def shard_bounds(m, n, world, rank):
     return (mo[rank], mo[rank + 1]), (no[rank], no[rank + 1])
 
 
+def _guard_int32(k_global, bits_a, bits_b):
+    """The int32 accumulators of an int8 product over a contraction of global length k_global
+    (summed exactly across ranks) must not wrap: k_global * cap_a * cap_b < 2^31 (the
+    single-GPU path routes such products through its exact int64 limb path instead; the
+    reference's own guard is the int64 rule, quant.py:87-93)."""
+    if k_global * bit_cap(bits_a) * bit_cap(bits_b) >= 2 ** 31:
+        raise OverflowRiskError(f"contraction length {k_global} with bit budgets ({bits_a}, {bits_b}) overflows the "
+                                "int32 accumulators of the sharded path")
+
+
 class _Sketch:
     """The products of the randomised SVD, fp64 (parity) or int8 (fast) with global scales."""
 
@@ -211,12 +223,14 @@ class _Sketch:
             self.comm.max_(amax)
         return amax
 
-    def product(self, x, y, bits, x_sharded, y_sharded, contract_sharded):
+    def product(self, x, y, bits, x_sharded, y_sharded, contract_sharded, k_global=None):
         """x (M x K) . y (K x N) where the K dimension may be split across ranks
-        (contract_sharded: the result is a partial sum to be allreduced)."""
+        (contract_sharded: the result is a partial sum to be allreduced; k_global = the full
+        contraction length)."""
         if bits is None:
             out = self.ops.gemm(0, x, y)
             return self.comm.sum_(out) if contract_sharded else out
+        _guard_int32(k_global or x.shape[1], bits, bits)
         lg = "row" if self.gran == "row" else "tensor"
         rg = "col" if self.gran == "row" else "tensor"
         ax = self._scales_amax(x, lg, x_sharded)
@@ -228,11 +242,12 @@ class _Sketch:
             self.comm.sum_(acc)  # int32 partials: exact
         return self.ops.dequant(acc, sx, sy)
 
-    def product_t(self, x, y, bits, x_sharded, y_sharded, contract_sharded):
+    def product_t(self, x, y, bits, x_sharded, y_sharded, contract_sharded, k_global=None):
         """x^T (K x M)^T . y (K x N) -> M x N, contraction over the rows of x and y."""
         if bits is None:
             out = self.ops.gemm(1, x, y)
             return self.comm.sum_(out) if contract_sharded else out
+        _guard_int32(k_global or x.shape[0], bits, bits)
         lg = "col" if self.gran == "row" else "tensor"  # columns of x are the rows of x^T
         rg = "col" if self.gran == "row" else "tensor"
         ax = self._scales_amax(x, lg, x_sharded)
@@ -274,6 +289,8 @@ def lramm_sharded(a_rows, b_cols, shape, params, comm=None, ops=None, c_rows=Non
     assert a_rows.shape == (mb - ma, k) and b_cols.shape == (k, nb - na)
     r = params.rank
     q_iters = params.power_iters
+    if max(params.bits) > 8:
+        raise UnsupportedError("the sharded path carries int8 operands: recombination bit budgets must be <= 8")
     sk = _Sketch(params, comm, ops)
     if params.mode != "fast":  # the reference works in fp64 throughout (matcore.py:62-70)
         a_rows, b_cols = a_rows.double(), b_cols.double()
@@ -285,11 +302,11 @@ def lramm_sharded(a_rows, b_cols, shape, params, comm=None, ops=None, c_rows=Non
     y = sk.product(a_rows, om_a, sk.sb, "rows", None, False)
     qa, _ = _cholqr2_rows(y, comm, ops)
     for _ in range(q_iters):
-        z = sk.product_t(a_rows, qa, sk.pb, "rows", "rows", True)  # A^T Q : k x w, summed over row shards
+        z = sk.product_t(a_rows, qa, sk.pb, "rows", "rows", True, k_global=m)  # A^T Q : k x w, summed over row shards
         qz = ops.qr(z)
         y = sk.product(a_rows, qz, sk.pb, "rows", None, False)
         qa, _ = _cholqr2_rows(y, comm, ops)
-    bst_a = sk.product_t(a_rows, qa, sk.jb, "rows", "rows", True)  # Bs^T = A^T Q (k x w)
+    bst_a = sk.product_t(a_rows, qa, sk.jb, "rows", "rows", True, k_global=m)  # Bs^T = A^T Q (k x w)
     v_a, s_a, h_a = ops.svd(bst_a)  # Bs^T = V S H^T  ->  u_Bs = H, v_Bs = V
     u_a = ops.gemm(0, qa, h_a[:, :r].contiguous())  # local rows of U_A
     v_a, s_a = v_a[:, :r].contiguous(), s_a[:r].contiguous()
@@ -298,12 +315,12 @@ def lramm_sharded(a_rows, b_cols, shape, params, comm=None, ops=None, c_rows=Non
     wb = sketch_width((k, n), r, params.oversample)
     om_b = ops.omega(seed_b, n, wb)
     om_bj = om_b[na:nb].contiguous()
-    yb = sk.product(b_cols, om_bj, sk.sb, "cols", "rows", True)  # B Omega = sum_j B_j Omega_j
+    yb = sk.product(b_cols, om_bj, sk.sb, "cols", "rows", True, k_global=n)  # B Omega = sum_j B_j Omega_j
     qb = ops.qr(yb)
     for _ in range(q_iters):
         zj = sk.product_t(b_cols, qb, sk.pb, "cols", None, False)  # local rows of B^T Q
         qzj, _ = _cholqr2_rows(zj, comm, ops)
-        yb = sk.product(b_cols, qzj, sk.pb, "cols", "rows", True)
+        yb = sk.product(b_cols, qzj, sk.pb, "cols", "rows", True, k_global=n)
         qb = ops.qr(yb)
     bst_bj = sk.product_t(b_cols, qb, sk.jb, "cols", None, False)  # local rows of Bs^T (n_j x w)
     _, rb = _cholqr2_rows(bst_bj, comm, ops, want_r=True)
@@ -315,6 +332,9 @@ def lramm_sharded(a_rows, b_cols, shape, params, comm=None, ops=None, c_rows=Non
 
     # ---- recombination (pipeline.py:188-210), per-tensor scales made global
     d1, d2, d3 = params.bits
+    _guard_int32(k, d1, d1)
+    _guard_int32(r, d2, d2)
+    _guard_int32(r, d3, d3)
     vt = v_a.T.contiguous()  # r x k, replicated
     e1 = _qgemm_replicated(vt, u_b, d1, ops)  # r x r, identical on every rank
     zsc_t = (v_bj * s_b).contiguous()  # n_j x r  (= Zsc^T local rows)

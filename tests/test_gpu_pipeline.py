@@ -3,7 +3,7 @@
 Gates:
   L2  recombination: given the same factors, E1 -> E2 -> E3 is bit-identical.
   L3  factorisation: sigma to 1e-10 relative, sign-invariant subspaces to 1e-9.
-  L4  parity mode end to end: <= 1e-3 relative Frobenius vs the reference's lramm()
+  L4  parity mode end to end: <= 1e-9 relative Frobenius vs the reference's lramm()
       (the reference's own two kernel backends differ by up to ~2e-3 on rare seeds:
       the chained per-tensor quantisers are discontinuous).
   L5  fast mode (int8 sketches): <= 1e-3 vs the CPU restatement at the same seeds,
@@ -24,7 +24,7 @@ torch = pytest.importorskip("torch")
 HERE = os.path.dirname(os.path.abspath(__file__))
 G = np.load(os.path.join(HERE, "golden", "reference_golden.npz"))
 sys.path.insert(0, os.path.join(HERE, "golden"))
-import make_golden as MG  # noqa: E402  (case tables only)
+import cases as MG  # noqa: E402  (case tables only; does not import the reference)
 
 
 @pytest.fixture(scope="module")
@@ -120,7 +120,10 @@ def test_lramm_parity_vs_reference_golden(L, idx):
     d, timings = L.lramm(a, b, L.LrammParams(rank=rank, bits=bits, power_iters=q_iters, oversample=p, seed=seed))
     assert d.dtype == np.float64 and d.shape == (m, n)
     ref = G[f"lr_{name}_pure"]
-    assert O.rel_fro(d, ref) <= 1e-3
+    # the reference's two kernel backends agree to <= 2.2e-13 on every one of these cases, so
+    # the gate is the SURVEY §8(c) L4 bound, 1e-9 (not the BASELINE 1e-3 target)
+    assert O.rel_fro(G[f"lr_{name}_compiled"], ref) <= 1e-12
+    assert O.rel_fro(d, ref) <= 1e-9
     assert set(timings.wall_ns) == set(L.STAGES)
 
 
@@ -131,6 +134,10 @@ def test_lramm_lowrank_inputs(L, idx):
     b = O.generate(k, n, "lowrank", seed + 100, rank=lr_rank)
     d, _ = L.lramm(a, b, L.LrammParams(rank=rank, bits=bits, power_iters=q_iters, oversample=p, seed=seed))
     exact = a @ b
+    spread = O.rel_fro(G[f"lr_{name}_compiled"], G[f"lr_{name}_pure"])
+    if spread <= 1e-12:  # the reference's backends agree: the L4 gate
+        assert O.rel_fro(d, G[f"lr_{name}_pure"]) <= 1e-9
+        return
     # rank-deficient operands (rank < params.rank): the trailing singular triplets are an
     # arbitrary orthonormal completion in the reference too (its LAPACK and Jacobi backends
     # pick different ones), and they enter E1's per-tensor scale.  Gate: accuracy vs the exact
@@ -143,9 +150,10 @@ def test_lramm_config1_parity(L):
     a = O.synth(1024, 1024, "exp:32", 1, 0, 0)
     b = O.synth(1024, 1024, "exp:32", 1, 0, 1)
     d, _ = L.lramm(a, b, L.LrammParams(rank=64, bits=(8, 8, 8), power_iters=1, oversample=10, seed=0))
-    assert abs(np.linalg.norm(d) - float(G["c1_fro"])) <= 1e-3 * float(G["c1_fro"])
-    assert O.rel_fro(d.sum(axis=1), G["c1_rowsum"]) <= 1e-3
-    assert O.rel_fro(d[:32, :32], G["c1_block"]) <= 1e-3
+    assert abs(np.linalg.norm(d) - float(G["c1_fro"])) <= 1e-9 * float(G["c1_fro"])
+    assert O.rel_fro(d.sum(axis=1), G["c1_rowsum"]) <= 1e-9
+    assert O.rel_fro(d.sum(axis=0), G["c1_colsum"]) <= 1e-9
+    assert O.rel_fro(d[:32, :32], G["c1_block"]) <= 1e-9
     exact = a.astype(np.float64) @ b.astype(np.float64)
     assert abs(O.rel_fro(d, exact) - float(G["c1_relerr_exact"])) <= 0.02 * float(G["c1_relerr_exact"])
 

@@ -111,7 +111,7 @@ def _load_mg():
     import sys
 
     sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
-    import make_golden as MG  # noqa: F401  (only the case tables are used)
+    import cases as MG  # noqa: F401  (only the case tables are used)
 
     return MG
 
