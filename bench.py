@@ -275,7 +275,8 @@ def reference_step(ref, a, b, cfg, sample_rows=E_SAMPLE_ROWS):
     import lramm.matcore as rm
     from lramm import _kernels as rk
     from lramm import quant as rq
-    from lramm import rsvd as rr
+    import lramm.rsvd  # noqa: F401
+    rr = sys.modules["lramm.rsvd"]  # the module: lramm re-exports the rsvd function under the same name
     from lramm.pipeline import _child_seeds
 
     r, q, p = cfg["rank"], cfg["power_iters"], cfg["oversample"]

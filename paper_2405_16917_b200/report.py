@@ -184,7 +184,9 @@ def leading_sigmas(a, count, seed=0):
     shape = _shape(a)
     if len(shape) != 2:
         raise ShapeError("matrix must be 2-D")
-    from . import rsvd as _rsvd  # the oracle cap (matcore.py:23), read at call time
+    import sys
+
+    _rsvd = sys.modules[__package__ + ".rsvd"]  # the module (the package re-exports the function); cap read at call time (matcore.py:23)
 
     if min(shape) <= _rsvd.ORACLE_MAX_MIN_DIM:
         return np.asarray(oracle_svd(a).sigma)[:count], "oracle"
