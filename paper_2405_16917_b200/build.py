@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "liblramm_cuda.so")
-SOURCES = ["quantize.cu", "igemm.cu", "dgemm.cu", "factor.cu", "pipeline.cu", "omega.cu", "api.cu"]
+SOURCES = ["quantize.cu", "igemm.cu", "dgemm.cu", "factor.cu", "eig.cu", "pipeline.cu", "omega.cu", "api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-DNDEBUG", f"-I{os.path.join(ROOT, 'include')}"]
 

@@ -1,0 +1,1284 @@
+// Eigenvector preconditioner for the one-sided Jacobi SVD (svd_tall_device, factor.cu).
+//
+// The reference computes the small SVD of the projection Bs (rsvd.py:78) with one-sided cyclic
+// Jacobi sweeps to tol 1e-13 (_jacobi.py:14-50, _core.pyx:72-133).  On the device that is a
+// chain of ~10 sweeps x (w - 1) dependent rotation steps.  Here the right singular vectors of
+// W = R^T are first obtained to working accuracy from the symmetric eigenproblem of the Gram
+// G = W^T W = R R^T, and W is rotated by them once (W' = W V0, V0 orthogonal) -- a Jacobi
+// preconditioner: W' has columns orthogonal to ~1e-15 relative, so the Jacobi run that follows
+// (same kernel, same tolerance, same convergence test) has nothing left to rotate and is
+// skipped by a device-side gate; when it is not (clustered / rank-deficient spectra, any failed
+// check), the same Jacobi runs on W' -- or on the untouched W when the preconditioner itself
+// failed -- and converges as before.  The singular values and left vectors are read from W'
+// exactly as from the Jacobi result (column norms, normalised columns), so the multiplicative
+// perturbation of an orthogonal V0 leaves them within ~eps relative (one-sided accuracy).
+//
+//   G = R R^T (DMMA GEMM)  ->  tridiagonalisation G = Q T Q^T      (sytrd_cluster_kernel)
+//   eigenvalues of T by multisection Sturm counts                  (tridiag_bisect_kernel)
+//   eigenvectors of T by one twisted factorisation each            (tridiag_twisted_kernel)
+//   Z <- Z (Z^T Z)^-1/2 to first order (Lowdin)                    (GEMMs + eig_defect_kernel)
+//   V0 = Q Z by the stored Householder reflectors                  (backtransform_kernel)
+//   P = W V0 ; E_ij = S_ij / (S_jj - S_ii), S = P^T P ; P <- P + P E   (one-sided refinement)
+//   gate = any S_ij^2 > tol^2 S_ii S_jj (S = P^T P)  -> Jacobi runs only if set
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace cg = cooperative_groups;
+
+#ifdef LRAMM_SYTRD_TRACE
+__device__ long long sytrd_trace[16];
+#define STR_MARK(v) long long v = clock64();
+#define STR_ADD(slot, a, b) \
+  if (threadIdx.x == 0 && blockIdx.x == 0) sytrd_trace[slot] += (b) - (a);
+#else
+#define STR_MARK(v)
+#define STR_ADD(slot, a, b)
+#endif
+
+namespace lramm {
+int dgemm_device_ex(int trans_a, int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B,
+                    int64_t ldb, double *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st,
+                    const DgemmOptions &opt);
+size_t dgemm_ws_bytes(int trans_a, int64_t M, int64_t N, int64_t K);
+int transpose_device(const double *a, int64_t rows, int64_t cols, int64_t lda, double *b, int64_t ldb,
+                     cudaStream_t st);
+
+using sm100::cp_async8;
+using sm100::cp_async_wait_all;
+namespace {
+
+// ------------------------------------------------------------------ CTA reductions
+template <int NW>
+__device__ __forceinline__ double cta_sum(double v, double *red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  const int nw = blockDim.x >> 5;
+  for (int i = 0; i < nw; ++i) s += red[i];
+  return s;
+}
+
+__device__ __forceinline__ double cta_max(double v, double *red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  const int nw = blockDim.x >> 5;
+  for (int i = 0; i < nw; ++i) s = fmax(s, red[i]);
+  return s;
+}
+
+// ------------------------------------------------------------------ tridiagonalisation
+// LAPACK dsytd2 (lower) semantics: reflector k = I - tau_k v_k v_k^T acts on indices k+1..n-1,
+// v_k[k+1] = 1; d_k = T_kk, e_k = T_{k+1,k} = beta_k.  Rows of the n x n matrix are spread
+// cyclically over the C CTAs of a cluster (row i on CTA i mod C, in shared memory).  Step k:
+//   every CTA knows v_k, tau_k (computed redundantly) and holds its rows of A_k;
+//   p_i = tau_k A_k[i, k+1:] . v_k for its rows i > k is published in its own shared memory
+//   together with (owner of row k+1) the trailing part of row k+1;
+//   one cluster barrier; every CTA gathers the whole of p and row k+1 through DSMEM, forms
+//   w = p - (tau_k/2)(p.v_k) v_k, updates row k+1 to A_{k+1} (redundantly) and derives
+//   reflector k+1 from it, then updates its own rows (A -= v w^T + w v^T) fused with the next
+//   dot products.  One cluster-wide exchange per step.
+struct SytrdArgs {
+  const double *G;  // n x n row-major (ldg), symmetric; problem stride g_stride
+  int64_t ldg, g_stride;
+  int n;
+  double *d, *e, *tau;  // per problem: n, n, n (stride n)
+  double *V;            // per problem n x n row-major: row k = v_k at columns k+1..n-1
+  int ldr;              // shared-memory row stride (doubles)
+};
+
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// reflector from x = (alpha, r[j0+1..n-1]): beta, tau, 1/(alpha - beta) (LAPACK dlarfg without the
+// rescaling loop; the operand is prescaled to an O(1) range)
+__device__ __forceinline__ void householder(double alpha, double s2, double &beta, double &tau, double &scl) {
+  if (s2 == 0.0) {
+    tau = 0.0;
+    beta = alpha;
+    scl = 0.0;
+  } else {
+    beta = -copysign(sqrt(fma(alpha, alpha, s2)), alpha);
+    tau = (beta - alpha) / beta;
+    scl = 1.0 / (alpha - beta);
+  }
+}
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ double ld_cluster_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+// E = elements per lane of a trailing row (n <= 32 E); every per-row loop is unrolled so its
+// shared-memory loads issue back to back.
+template <int E>
+__global__ void __launch_bounds__(640, 1) sytrd_cluster_kernel(SytrdArgs a) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = (int)cl.num_blocks();  // a power of two
+  const int lgC = __ffs(C) - 1;
+  const int me = (int)cl.block_rank();
+  const int prob = blockIdx.x >> lgC;
+  const int n = a.n, ldr = a.ldr;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5, nth = blockDim.x;
+  const int nl = (n - me + C - 1) >> lgC;  // local rows: global i = me + li * C
+  const int nlmax = (n + C - 1) >> lgC;
+  extern __shared__ __align__(16) double sm[];
+  double2 *pub = reinterpret_cast<double2 *>(sm);              // [2][nlmax] (p_i, a_{i,k+1})
+  double *A = sm + 4 * nlmax;                                  // [nlmax][ldr]
+  double *pf = A + (size_t)nlmax * ldr;                        // [ldr] gathered p
+  double *rk = pf + ldr;                                       // [ldr] gathered column k+1 (= row k+1)
+  double *vb = rk + ldr;                                       // [2][ldr] reflectors (current / next)
+  __shared__ double red[2][32];
+  __shared__ double hh[4];  // tau_{k+1}
+
+  const double *G = a.G + (size_t)prob * a.g_stride;
+  double *dout = a.d + (size_t)prob * n, *eout = a.e + (size_t)prob * n, *tout = a.tau + (size_t)prob * n;
+  double *Vout = a.V + (size_t)prob * n * n;
+
+  // exact power-of-two prescale: largest diagonal into [1, 4)
+  double dm = 0.0;
+  for (int i = tid; i < n; i += nth) dm = fmax(dm, fabs(G[(int64_t)i * a.ldg + i]));
+  dm = cta_max(dm, red[0]);
+  double scale = 1.0;
+  if (dm > 0.0 && dm <= DBL_MAX) scale = ldexp(1.0, -2 * (ilogb(dm) >> 1));
+  for (int li = warp; li < nl; li += nwarp) {
+    const int i = me + (li << lgC);
+    const double *src = G + (int64_t)i * a.ldg;
+    for (int j = lane; j < n; j += 32) A[(size_t)li * ldr + j] = src[j] * scale;
+  }
+  for (int j = tid; j < n; j += nth) rk[j] = G[j] * scale;
+  __syncthreads();
+  double *v = vb, *vn = vb + ldr;
+  double tau;
+  {  // row 0 (redundant in every CTA) -> d_0, reflector 0
+    double s2 = 0.0;
+    for (int j = 2 + tid; j < n; j += nth) s2 = fma(rk[j], rk[j], s2);
+    s2 = cta_sum<32>(s2, red[1]);
+    double beta, scl;
+    householder(rk[1], s2, beta, tau, scl);
+    for (int j = 1 + tid; j < n; j += nth) {
+      const double vj = j == 1 ? 1.0 : rk[j] * scl;
+      v[j] = vj;
+      if (me == 0) Vout[j] = vj;
+    }
+    if (me == 0 && tid == 0) {
+      dout[0] = rk[0];
+      eout[0] = beta;
+      tout[0] = tau;
+    }
+  }
+  __syncthreads();
+  {  // p_0 and column-1 entries of own rows i >= 1
+    for (int li = warp; li < nl; li += nwarp) {
+      const int i = me + (li << lgC);
+      if (i < 1) continue;
+      const double *ar = A + (size_t)li * ldr;
+      double dot = 0.0;
+      for (int j = 1 + lane; j < n; j += 32) dot = fma(ar[j], v[j], dot);
+      dot = warp_allsum(dot);
+      if (lane == 0) pub[li] = make_double2(tau * dot, ar[1]);
+    }
+  }
+  const uint32_t pub_s = sm100::smem_u32(pub);
+  cl.sync();
+
+  for (int k = 0; k <= n - 3; ++k) {
+    const int par = k & 1, npar = par ^ 1;
+    const bool last = (k == n - 3);
+    STR_MARK(t0);
+    // ---- gather (p_j, A_k[j, k+1]) for j = k+1..n-1 through DSMEM (row j lives on CTA j mod C)
+    for (int j = k + 1 + tid; j < n; j += nth) {
+      const uint32_t pa = mapa_u32(pub_s + (par * nlmax + (j >> lgC)) * 16, j & (C - 1));
+      double pj, cj;
+      asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(pj), "=d"(cj) : "r"(pa) : "memory");
+      pf[j] = pj;
+      rk[j] = cj;
+    }
+    __syncthreads();
+    STR_MARK(t1);
+    // ---- s = p . v (every warp, redundantly); w_j = p_j - c v_j
+    const int j0 = k + 1 + lane;  // this lane's columns: j0 + 32 e
+    double pr[E], vr[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int j = j0 + 32 * e;
+      const bool in = j < n;
+      pr[e] = in ? pf[j] : 0.0;
+      vr[e] = in ? v[j] : 0.0;
+    }
+    double sacc = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) sacc = fma(pr[e], vr[e], sacc);
+    const double c = 0.5 * tau * warp_allsum(sacc);
+    const double wk1 = __shfl_sync(0xffffffffu, pr[0], 0) - c;  // p_{k+1} - c v_{k+1}, v_{k+1} == 1
+    STR_MARK(t2);
+    if (warp == 0) {
+      // ---- row k+1 of A_{k+1}, d_{k+1}, reflector k+1 (warp 0; other warps update rows)
+      double r[E];
+      double s2 = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int j = j0 + 32 * e;
+        const double rkj = j < n ? rk[j] : 0.0;
+        r[e] = rkj - fma(-c, vr[e], pr[e]) - wk1 * vr[e];
+        if (j >= k + 3 && j < n) s2 = fma(r[e], r[e], s2);
+      }
+      s2 = warp_allsum(s2);
+      const double alpha = __shfl_sync(0xffffffffu, r[0], 1);  // j = k+2
+      const double dk1 = __shfl_sync(0xffffffffu, r[0], 0);    // j = k+1
+      if (!last) {
+        double beta, tn, scl;
+        householder(alpha, s2, beta, tn, scl);
+        double *vrow = Vout + (size_t)(k + 1) * n;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int j = j0 + 32 * e;
+          if (j >= k + 2 && j < n) {
+            const double vj = j == k + 2 ? 1.0 : r[e] * scl;
+            vn[j] = vj;
+            if (me == 0) vrow[j] = vj;
+          }
+        }
+        if (lane == 0) {
+          hh[0] = tn;
+          if (me == 0) {
+            dout[k + 1] = dk1;
+            eout[k + 1] = beta;
+            tout[k + 1] = tn;
+          }
+        }
+      } else if (me == 0 && lane == 0) {
+        dout[n - 2] = dk1;
+        eout[n - 2] = alpha;
+      }
+    } else {
+      // ---- own rows i >= k+2: A -= v w^T + w v^T (columns >= k+1 of the lane layout; the
+      //      column k+1 entry is never read again)
+      int li0 = (k + 2 - me + C - 1) >> lgC;
+      if (li0 < 0) li0 = 0;
+      for (int li = li0 + warp - 1; li < nl; li += nwarp - 1) {
+        const int i = me + (li << lgC);
+        double *ar = A + (size_t)li * ldr;
+        const double vi = v[i], wi = pf[i] - c * vi;
+        double x[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int j = j0 + 32 * e;
+          x[e] = j < n ? ar[j] : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int j = j0 + 32 * e;
+          const double wj = fma(-c, vr[e], pr[e]);
+          const double xv = fma(-wi, vr[e], fma(-vi, wj, x[e]));
+          if (j < n) ar[j] = xv;
+        }
+        if (last && i == n - 1 && lane == 1) dout[n - 1] = ar[n - 1];  // j0 + 0 == n - 1 on lane 1
+      }
+    }
+    if (last) break;
+    STR_MARK(t3);
+    __syncthreads();
+    STR_MARK(t4);
+    // ---- p_{k+1} and the column-(k+2) entry of own rows i >= k+2
+    {
+      const double tn = hh[0];
+      double vv[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int j = j0 + 32 * e;
+        vv[e] = (j >= k + 2 && j < n) ? vn[j] : 0.0;
+      }
+      int li0 = (k + 2 - me + C - 1) >> lgC;
+      if (li0 < 0) li0 = 0;
+      for (int li = li0 + warp; li < nl; li += nwarp) {
+        const double *ar = A + (size_t)li * ldr;
+        double dot = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int j = j0 + 32 * e;
+          dot = fma(j < n ? ar[j] : 0.0, vv[e], dot);
+        }
+        dot = warp_allsum(dot);
+        if (lane == 0) pub[npar * nlmax + li] = make_double2(tn * dot, ar[k + 2]);
+      }
+      tau = tn;
+    }
+    {
+      double *t = v;
+      v = vn;
+      vn = t;
+    }
+    STR_MARK(t5);
+    cl.sync();
+    STR_MARK(t6);
+    STR_ADD(0, t0, t1);
+    STR_ADD(1, t1, t2);
+    STR_ADD(2, t2, t3);
+    STR_ADD(3, t3, t4);
+    STR_ADD(4, t4, t5);
+    STR_ADD(5, t5, t6);
+    STR_ADD(6, t0, t6);
+  }
+  cl.sync();  // peers may still be reading this CTA's shared memory
+}
+
+// Register-resident variant (n <= 32 * kSytrdRegMaxE): each row warp keeps up to RMAX rows of
+// the CTA in registers (lane owns columns lane + 32 e), so a step touches shared memory only
+// for the gathered vectors.  Warp 0 derives the reflector (as above); warps 1.. update their
+// rows (inactive columns carry p = v = 0, so the rank-2 update leaves them unchanged) and form
+// the next dot products from registers.
+constexpr int kSytrdRegMaxE = 12;
+__host__ __device__ constexpr int sytrd_rmax(int e) { return 96 / e - 2 > 24 ? 24 : 96 / e - 2; }
+
+template <int E>
+__global__ void __launch_bounds__(256, 1) sytrd_reg_kernel(SytrdArgs a) {
+  constexpr int RM = sytrd_rmax(E);
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = (int)cl.num_blocks();  // a power of two
+  const int lgC = __ffs(C) - 1;
+  const int me = (int)cl.block_rank();
+  const int prob = blockIdx.x >> lgC;
+  const int n = a.n, ldr = a.ldr;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5, nth = blockDim.x;
+  const int nrw = nwarp - 1;                 // row warps
+  const int nl = (n - me + C - 1) >> lgC;   // local rows: global i = me + li * C
+  const int nlmax = (n + C - 1) >> lgC;
+  extern __shared__ __align__(16) double sm[];
+  double2 *pub = reinterpret_cast<double2 *>(sm);  // [2][nlmax] (p_i, a_{i,k+1})
+  double *pf = sm + 4 * nlmax;                     // [ldr] gathered p
+  double *rk = pf + ldr;                           // [ldr] gathered column k+1 (= row k+1)
+  double *vb = rk + ldr;                           // [2][ldr] reflectors (current / next)
+  __shared__ double red[2][32];
+  __shared__ double hh[4];
+
+  const double *G = a.G + (size_t)prob * a.g_stride;
+  double *dout = a.d + (size_t)prob * n, *eout = a.e + (size_t)prob * n, *tout = a.tau + (size_t)prob * n;
+  double *Vout = a.V + (size_t)prob * n * n;
+
+  double dm = 0.0;
+  for (int i = tid; i < n; i += nth) dm = fmax(dm, fabs(G[(int64_t)i * a.ldg + i]));
+  dm = cta_max(dm, red[0]);
+  double scale = 1.0;
+  if (dm > 0.0 && dm <= DBL_MAX) scale = ldexp(1.0, -2 * (ilogb(dm) >> 1));
+  // rows of this warp: li = (warp - 1) + r * nrw
+  double x[RM][E];
+  int gi[RM];
+#pragma unroll
+  for (int r = 0; r < RM; ++r) {
+    const int li = warp - 1 + r * nrw;
+    gi[r] = (warp >= 1 && li < nl) ? me + (li << lgC) : -1;
+    const double *src = G + (int64_t)(gi[r] < 0 ? 0 : gi[r]) * a.ldg;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int j = lane + 32 * e;
+      x[r][e] = (gi[r] >= 0 && j < n) ? src[j] * scale : 0.0;
+    }
+  }
+  for (int j = tid; j < n; j += nth) rk[j] = G[j] * scale;
+  __syncthreads();
+  double *v = vb, *vn = vb + ldr;
+  double tau;
+  {  // row 0 (redundant in every CTA) -> d_0, reflector 0
+    double s2 = 0.0;
+    for (int j = 2 + tid; j < n; j += nth) s2 = fma(rk[j], rk[j], s2);
+    s2 = cta_sum<32>(s2, red[1]);
+    double beta, scl;
+    householder(rk[1], s2, beta, tau, scl);
+    for (int j = tid; j < n; j += nth) {
+      const double vj = j < 1 ? 0.0 : (j == 1 ? 1.0 : rk[j] * scl);
+      v[j] = vj;
+      if (me == 0 && j >= 1) Vout[j] = vj;
+    }
+    if (me == 0 && tid == 0) {
+      dout[0] = rk[0];
+      eout[0] = beta;
+      tout[0] = tau;
+    }
+  }
+  __syncthreads();
+  {  // p_0 and the column-1 entries of own rows i >= 1
+    double vv[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int j = lane + 32 * e;
+      vv[e] = j < n ? v[j] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < RM; ++r) {
+      double dot = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) dot = fma(x[r][e], vv[e], dot);
+      dot = warp_allsum(dot);
+      const double c1 = __shfl_sync(0xffffffffu, x[r][0], 1);
+      if (gi[r] >= 1 && lane == 0) pub[(gi[r] >> lgC)] = make_double2(tau * dot, c1);
+    }
+  }
+  const uint32_t pub_s = sm100::smem_u32(pub);
+  cl.sync();
+
+  for (int k = 0; k <= n - 3; ++k) {
+    const int par = k & 1, npar = par ^ 1;
+    const bool last = (k == n - 3);
+    for (int j = k + 1 + tid; j < n; j += nth) {
+      const uint32_t pa = mapa_u32(pub_s + (par * nlmax + (j >> lgC)) * 16, j & (C - 1));
+      double pj, cj;
+      asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(pj), "=d"(cj) : "r"(pa) : "memory");
+      pf[j] = pj;
+      rk[j] = cj;
+    }
+    __syncthreads();
+    // w_j = p_j - c v_j on this lane's columns (zero for j <= k)
+    double wr[E], vr[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int j = lane + 32 * e;
+      const bool in = j > k && j < n;
+      wr[e] = in ? pf[j] : 0.0;
+      vr[e] = in ? v[j] : 0.0;
+    }
+    double sacc = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) sacc = fma(wr[e], vr[e], sacc);
+    const double c = 0.5 * tau * warp_allsum(sacc);
+#pragma unroll
+    for (int e = 0; e < E; ++e) wr[e] = fma(-c, vr[e], wr[e]);
+    if (warp == 0) {
+      // ---- column k+1 of A_{k+1}: r_j = A_k[j,k+1] - v_j w_{k+1} - w_j (v_{k+1} = 1)
+      const double wk1 = pf[k + 1] - c;
+      double rr[E];
+      double s2 = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int j = lane + 32 * e;
+        rr[e] = (j > k && j < n) ? rk[j] - wr[e] - wk1 * vr[e] : 0.0;
+        if (j >= k + 3) s2 = fma(rr[e], rr[e], s2);
+      }
+      s2 = warp_allsum(s2);
+      // alpha = r_{k+2}, d_{k+1} = r_{k+1}: from the owning lanes
+      double al = 0.0, dk = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (e == ((k + 2) >> 5)) al = rr[e];
+        if (e == ((k + 1) >> 5)) dk = rr[e];
+      }
+      const double alpha = __shfl_sync(0xffffffffu, al, (k + 2) & 31);
+      const double dk1 = __shfl_sync(0xffffffffu, dk, (k + 1) & 31);
+      if (!last) {
+        double beta, tn, scl;
+        householder(alpha, s2, beta, tn, scl);
+        double *vrow = Vout + (size_t)(k + 1) * n;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int j = lane + 32 * e;
+          if (j < n) {
+            const double vj = j < k + 2 ? 0.0 : (j == k + 2 ? 1.0 : rr[e] * scl);
+            vn[j] = vj;
+            if (me == 0 && j >= k + 2) vrow[j] = vj;
+          }
+        }
+        if (lane == 0) {
+          hh[0] = tn;
+          if (me == 0) {
+            dout[k + 1] = dk1;
+            eout[k + 1] = beta;
+            tout[k + 1] = tn;
+          }
+        }
+      } else if (me == 0 && lane == 0) {
+        dout[n - 2] = dk1;
+        eout[n - 2] = alpha;
+      }
+    } else {
+      // ---- own rows i >= k+2 in registers: A -= v w^T + w v^T
+#pragma unroll
+      for (int r = 0; r < RM; ++r) {
+        if (gi[r] >= k + 2) {
+          const double vi = v[gi[r]], wi = pf[gi[r]] - c * vi;
+#pragma unroll
+          for (int e = 0; e < E; ++e) x[r][e] = fma(-wi, vr[e], fma(-vi, wr[e], x[r][e]));
+        }
+      }
+      if (last) {
+#pragma unroll
+        for (int r = 0; r < RM; ++r)
+          if (gi[r] == n - 1) {
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+              if (lane + 32 * e == n - 1) dout[n - 1] = x[r][e];
+          }
+      }
+    }
+    if (last) break;
+    __syncthreads();
+    // ---- p_{k+1} and the column-(k+2) entry of own rows i >= k+2
+    const double tn = hh[0];
+    if (warp >= 1) {
+      double vv[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int j = lane + 32 * e;
+        vv[e] = j < n ? vn[j] : 0.0;  // zero below k+2 by construction
+      }
+      double dots[RM], cols[RM];
+#pragma unroll
+      for (int r = 0; r < RM; ++r) {
+        double dot = 0.0, ce = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          dot = fma(x[r][e], vv[e], dot);
+          if (e == ((k + 2) >> 5)) ce = x[r][e];
+        }
+        dots[r] = dot;
+        cols[r] = ce;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int r = 0; r < RM; ++r) dots[r] += __shfl_xor_sync(0xffffffffu, dots[r], o);
+      }
+#pragma unroll
+      for (int r = 0; r < RM; ++r) {
+        const double ck2 = __shfl_sync(0xffffffffu, cols[r], (k + 2) & 31);
+        if (gi[r] >= k + 2 && lane == 0) pub[npar * nlmax + (gi[r] >> lgC)] = make_double2(tn * dots[r], ck2);
+      }
+    }
+    tau = tn;
+    {
+      double *t = v;
+      v = vn;
+      vn = t;
+    }
+    cl.sync();
+  }
+  cl.sync();  // peers may still be reading this CTA's shared memory
+}
+
+// ------------------------------------------------------------------ eigenvalues of T
+// Multisection on Sturm counts: one warp per eigenvalue index i (ascending), each lane follows
+// NCH shifts; a round splits the bracket into 32*NCH+1 parts.  Counts come from the
+// leading-minor recurrence p_j = (d_j - x) p_{j-1} - e_{j-1}^2 p_{j-2} (no division; the
+// critical path per step is one FMA), rescaled by a power of two every 8 steps; the count is
+// the number of sign changes (sign bits; an exact zero is vanishingly rare at these shifts and
+// only moves the bracket by the point spacing).
+constexpr int kBisNCH = 2;
+constexpr int kBisRounds = 9;  // (32 * 2 + 1)^9 > 2^54
+
+__device__ __forceinline__ int sgnbit(double x) { return (int)((unsigned)__double2hiint(x) >> 31); }
+__device__ __forceinline__ int bexp(double x) { return (__double2hiint(x) >> 20) & 0x7ff; }
+
+__global__ void __launch_bounds__(256) tridiag_bisect_kernel(const double *__restrict__ dall,
+                                                             const double *__restrict__ eall, int n,
+                                                             double *__restrict__ lamall) {
+  extern __shared__ __align__(16) double sh[];
+  double2 *sde = reinterpret_cast<double2 *>(sh);  // (d_j, e_{j-1}^2)
+  __shared__ double red[32];
+  const int prob = blockIdx.y;
+  const double *d = dall + (size_t)prob * n, *e = eall + (size_t)prob * n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double lo_b = DBL_MAX, hi_b = -DBL_MAX;
+  for (int j = tid; j < n; j += blockDim.x) {
+    const double dj = d[j];
+    const double el = j > 0 ? fabs(e[j - 1]) : 0.0, er = j < n - 1 ? fabs(e[j]) : 0.0;
+    sde[j] = make_double2(dj, j > 0 ? e[j - 1] * e[j - 1] : 0.0);
+    lo_b = fmin(lo_b, dj - el - er);
+    hi_b = fmax(hi_b, dj + el + er);
+  }
+  lo_b = -cta_max(-lo_b, red);
+  __syncthreads();
+  hi_b = cta_max(hi_b, red);
+  const double span = fmax(hi_b - lo_b, DBL_MIN);
+  lo_b -= 4.0 * DBL_EPSILON * span + DBL_MIN;
+  hi_b += 4.0 * DBL_EPSILON * span + DBL_MIN;
+  const int i = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (i >= n) return;
+  double lo = lo_b, hi = hi_b;
+  constexpr int NP = 32 * kBisNCH;  // interior points per round
+  for (int round = 0; round < kBisRounds; ++round) {
+    double nx[kBisNCH], p1[kBisNCH], p2[kBisNCH];
+    int cnt[kBisNCH], ng[kBisNCH];
+    const double h = (hi - lo) / (double)(NP + 1);
+    const double d0 = sde[0].x;
+#pragma unroll
+    for (int t = 0; t < kBisNCH; ++t) {
+      nx[t] = -fma((double)(1 + lane + 32 * t), h, lo);
+      p2[t] = 1.0;
+      p1[t] = d0 + nx[t];
+      ng[t] = sgnbit(p1[t]);
+      cnt[t] = ng[t];
+    }
+#pragma unroll 8
+    for (int j = 1; j < n; ++j) {
+      const double2 de = sde[j];
+#pragma unroll
+      for (int t = 0; t < kBisNCH; ++t) {
+        const double pn = fma(de.x + nx[t], p1[t], -de.y * p2[t]);
+        const int g = sgnbit(pn);
+        cnt[t] += g ^ ng[t];
+        ng[t] = g;
+        p2[t] = p1[t];
+        p1[t] = pn;
+      }
+      if ((j & 7) == 0) {
+#pragma unroll
+        for (int t = 0; t < kBisNCH; ++t) {
+          // scale both by 2^-(e - 1023), e = the larger biased exponent (exact; |e - 1023| < 1023)
+          const int ex = max(bexp(p1[t]), bexp(p2[t]));
+          const double f = __hiloint2double((2046 - ex) << 20, 0);
+          p1[t] *= f;
+          p2[t] *= f;
+        }
+      }
+    }
+    int m = 0;  // points with count <= i (monotone in the point index)
+#pragma unroll
+    for (int t = 0; t < kBisNCH; ++t) m += __popc(__ballot_sync(0xffffffffu, cnt[t] <= i));
+    const double nlo = m >= 1 ? fma((double)m, h, lo) : lo;
+    const double nhi = m < NP ? fma((double)(m + 1), h, lo) : hi;
+    lo = nlo;
+    hi = fmax(nhi, nlo);
+  }
+  if (lane == 0) lamall[(size_t)prob * n + i] = 0.5 * (lo + hi);
+}
+
+// ------------------------------------------------------------------ eigenvectors of T
+// 1/x to ~1 ulp: MUFU reciprocal seed + two Newton steps (x normal, |x| >= pivmin)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// One thread per eigenvalue: stationary (L+ D+ L+^T) and progressive (U- D- U-^T) factorisations
+// of T - lambda I, twist index r = argmin |gamma_r|, gamma_r = D+_r + D-_r - (d_r - lambda);
+// z_r = 1, z_j = -L+_j z_{j+1} (j < r), z_{j+1} = -U-_{j+1} z_j (j >= r); normalised.
+// The multipliers of the CTA's threads live in shared memory laid out [j][thread]; T in shared
+// memory too.  The eigenvector is written as column i of Z (row-major n x n).
+__global__ void __launch_bounds__(32) tridiag_twisted_kernel(const double *__restrict__ dall,
+                                                             const double *__restrict__ eall, int n,
+                                                             const double *__restrict__ lamall,
+                                                             double *__restrict__ Zall) {
+  extern __shared__ __align__(16) double tw[];
+  const int nt = blockDim.x;
+  double *sd = tw, *se = tw + n;                 // d, e
+  double *Lp = se + n, *Um = Lp + (size_t)n * nt;  // [j][nt]
+  const int prob = blockIdx.y;
+  const double *d = dall + (size_t)prob * n, *e = eall + (size_t)prob * n;
+  double emax = 0.0;
+  for (int j = threadIdx.x; j < n; j += nt) {
+    sd[j] = d[j];
+    se[j] = j < n - 1 ? e[j] : 0.0;
+  }
+  __syncthreads();
+  for (int j = 0; j < n - 1; ++j) emax = fmax(emax, fabs(se[j]));
+  const int i = blockIdx.x * nt + threadIdx.x;
+  if (i >= n) return;
+  const int tx = threadIdx.x;
+  const double lam = lamall[(size_t)prob * n + i];
+  double *Z = Zall + (size_t)prob * n * n;
+  const double pivmin = DBL_MIN * fmax(1.0, emax * emax);
+  // forward D+ / L+ and backward D- / U-, interleaved (independent division chains)
+  double dp = sd[0] - lam, dmn = sd[n - 1] - lam;
+  for (int j = 0; j < n - 1; ++j) {
+    if (fabs(dp) < pivmin) dp = -pivmin;
+    const double l = se[j] * rcp_nr(dp);
+    Lp[(size_t)j * nt + tx] = l;
+    dp = (sd[j + 1] - lam) - l * se[j];
+    const int jb = n - 2 - j;
+    if (fabs(dmn) < pivmin) dmn = -pivmin;
+    const double u = se[jb] * rcp_nr(dmn);
+    Um[(size_t)(jb + 1) * nt + tx] = u;
+    dmn = (sd[jb] - lam) - u * se[jb];
+  }
+  // gamma_r = (d_r - lam) - L+_{r-1} e_{r-1} - U-_{r+1} e_r
+  int r = 0;
+  double gbest = DBL_MAX;
+  for (int j = 0; j < n; ++j) {
+    double g = sd[j] - lam;
+    if (j > 0) g -= Lp[(size_t)(j - 1) * nt + tx] * se[j - 1];
+    if (j < n - 1) g -= Um[(size_t)(j + 1) * nt + tx] * se[j];
+    if (fabs(g) < gbest) {
+      gbest = fabs(g);
+      r = j;
+    }
+  }
+  // vector (unnormalised; the components reuse the multiplier slots), then scaled into Z
+  double nrm2 = 1.0, z = 1.0;
+  for (int j = r - 1; j >= 0; --j) {
+    z = -Lp[(size_t)j * nt + tx] * z;
+    if (!(fabs(z) <= 1e150)) z = 0.0;  // guard runaway growth from an unusable pivot
+    Lp[(size_t)j * nt + tx] = z;
+    nrm2 = fma(z, z, nrm2);
+  }
+  z = 1.0;
+  for (int j = r; j < n - 1; ++j) {
+    z = -Um[(size_t)(j + 1) * nt + tx] * z;
+    if (!(fabs(z) <= 1e150)) z = 0.0;
+    Um[(size_t)(j + 1) * nt + tx] = z;
+    nrm2 = fma(z, z, nrm2);
+  }
+  const double inv = 1.0 / sqrt(nrm2);
+  for (int j = 0; j < n; ++j) {
+    const double zj = j < r ? Lp[(size_t)j * nt + tx] : (j == r ? 1.0 : Um[(size_t)j * nt + tx]);
+    Z[(size_t)j * n + i] = zj * inv;
+  }
+}
+
+// ------------------------------------------------------------------ checks and small updates
+// D <- Z^T Z - I in place; flags[0] |= (max |D| > limit or non-finite)
+__global__ void eig_defect_kernel(double *__restrict__ D, int n, int64_t stride, double limit, int *flags) {
+  const int prob = blockIdx.y;
+  double *Dp = D + (size_t)prob * stride;
+  bool bad = false;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)n * n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(t / n), c = (int)(t % n);
+    double x = Dp[t];
+    if (r == c) x -= 1.0;
+    Dp[t] = x;
+    if (!(fabs(x) <= limit)) bad = true;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags + prob * 4, 1);
+}
+
+// V0 = Q Z, Q = H_0 H_1 ... H_{n-3}, applied in WY blocks of kNB reflectors:
+//   H_{k0} ... H_{k0+nb-1} = I - V_b T_b V_b^T   (T_b upper triangular, reflector_t_kernel)
+//   Z <- Z - V_b (T_b (V_b^T Z)) for the blocks from last to first, on strips of kBtCols
+//   columns of Z held in shared memory (backtransform_kernel).
+constexpr int kNB = 32;
+constexpr int kBtCols = 8;
+
+// T_b of every block (one CTA each): G_ac = v_a . v_c (a < c), then row a of T by the forward
+// recurrence T[a][c] = -tau_c sum_{a <= b < c} T[a][b] G_bc, T[a][a] = tau_a
+__global__ void __launch_bounds__(256) reflector_t_kernel(const double *__restrict__ Vall,
+                                                          const double *__restrict__ tauall, int n,
+                                                          double *__restrict__ Tall) {
+  extern __shared__ __align__(16) double vs[];  // [kNB][n - k0]
+  __shared__ double Gs[kNB][kNB + 1];
+  __shared__ double Ts[kNB][kNB + 1];
+  const int prob = blockIdx.y, blk = blockIdx.x;
+  const int nblk = (n - 2 + kNB - 1) / kNB;
+  const double *V = Vall + (size_t)prob * n * n;
+  const double *tau = tauall + (size_t)prob * n;
+  double *T = Tall + ((size_t)prob * nblk + blk) * kNB * kNB;
+  const int k0 = blk * kNB, nb = min(kNB, n - 2 - k0), len = n - k0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  for (int t = tid; t < kNB * len; t += blockDim.x) {
+    const int r = t / len, j = t % len;
+    vs[t] = r < nb ? V[(size_t)(k0 + r) * n + k0 + j] : 0.0;  // zeros left of each vector's start
+  }
+  __syncthreads();
+  for (int pr = warp; pr < kNB * kNB; pr += nwarp) {
+    const int aa = pr / kNB, cc = pr % kNB;
+    if (aa >= cc || cc >= nb) continue;
+    const double *va = vs + (size_t)aa * len, *vc = vs + (size_t)cc * len;
+    double sacc = 0.0;
+    for (int j = cc + 1 + lane; j < len; j += 32) sacc = fma(va[j], vc[j], sacc);
+    sacc = warp_allsum(sacc);
+    if (lane == 0) Gs[aa][cc] = sacc;
+  }
+  __syncthreads();
+  if (tid < kNB) {
+    const int ar = tid;
+    for (int c = 0; c < kNB; ++c) Ts[ar][c] = 0.0;
+    if (ar < nb) {
+      Ts[ar][ar] = tau[k0 + ar];
+      for (int c = ar + 1; c < nb; ++c) {
+        double acc = 0.0;
+        for (int bb = ar; bb < c; ++bb) acc = fma(Ts[ar][bb], Gs[bb][c], acc);
+        Ts[ar][c] = -tau[k0 + c] * acc;
+      }
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < kNB * kNB; t += blockDim.x) T[t] = Ts[t / kNB][t % kNB];
+}
+
+// identity when the preconditioner failed (flags[0] != 0)
+__global__ void __launch_bounds__(256) backtransform_kernel(const double *__restrict__ Zall,
+                                                            const double *__restrict__ Vall,
+                                                            const double *__restrict__ Tall, int n,
+                                                            const int *__restrict__ flags,
+                                                            double *__restrict__ V0all) {
+  extern __shared__ __align__(16) double zs[];  // [n][kBtCols], then vsb[kNB][n] (block rows)
+  double *vsb = zs + (size_t)n * kBtCols;
+  __shared__ double w1[kNB][kBtCols];
+  __shared__ double w2[kNB][kBtCols];
+  __shared__ double ts[kNB][kNB + 1];
+  const int prob = blockIdx.y;
+  const int nblk = (n - 2 + kNB - 1) / kNB;
+  const double *Z = Zall + (size_t)prob * n * n;
+  const double *V = Vall + (size_t)prob * n * n;
+  const double *Tb = Tall + (size_t)prob * nblk * kNB * kNB;
+  double *V0 = V0all + (size_t)prob * n * n;
+  const int c0 = blockIdx.x * kBtCols;
+  const int tid = threadIdx.x;
+  const bool bad = flags[prob * 4] != 0;
+  if (bad) {
+    for (int t = tid; t < n * kBtCols; t += blockDim.x) {
+      const int j = t / kBtCols, c = c0 + t % kBtCols;
+      if (c < n) V0[(size_t)j * n + c] = (j == c) ? 1.0 : 0.0;
+    }
+    return;
+  }
+  for (int t = tid; t < n * kBtCols; t += blockDim.x) {
+    const int j = t / kBtCols, c = c0 + t % kBtCols;
+    zs[t] = c < n ? Z[(size_t)j * n + c] : 0.0;
+  }
+  const int sc = tid % kBtCols, rc = tid / kBtCols;  // 256 threads: 32 x kBtCols
+  for (int blk = nblk - 1; blk >= 0; --blk) {
+    const int k0 = blk * kNB, nb = min(kNB, n - 2 - k0);
+    for (int t = tid; t < kNB * kNB; t += blockDim.x) ts[t / kNB][t % kNB] = Tb[(size_t)blk * kNB * kNB + t];
+    for (int t = tid; t < nb * n; t += blockDim.x) {  // rows k0..k0+nb-1 of V (zero left of k0+r+1)
+      const int r = t / n, j = t % n;
+      vsb[t] = j > k0 + r ? V[(size_t)(k0 + r) * n + j] : 0.0;
+    }
+    __syncthreads();
+    // W1[c][s] = v_{k0+c} . Z[:, s]  (v_{k0+c} nonzero from k0+c+1)
+    {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if (rc < nb) {
+        const double *vr = vsb + (size_t)rc * n;
+        int j = k0 + rc + 1;
+        for (; j + 3 < n; j += 4) {
+          a0 = fma(vr[j], zs[j * kBtCols + sc], a0);
+          a1 = fma(vr[j + 1], zs[(j + 1) * kBtCols + sc], a1);
+          a2 = fma(vr[j + 2], zs[(j + 2) * kBtCols + sc], a2);
+          a3 = fma(vr[j + 3], zs[(j + 3) * kBtCols + sc], a3);
+        }
+        for (; j < n; ++j) a0 = fma(vr[j], zs[j * kBtCols + sc], a0);
+      }
+      w1[rc][sc] = (a0 + a1) + (a2 + a3);
+    }
+    __syncthreads();
+    // W2 = T_b W1
+    {
+      double acc = 0.0;
+      for (int c = rc; c < nb; ++c) acc = fma(ts[rc][c], w1[c][sc], acc);
+      w2[rc][sc] = acc;
+    }
+    __syncthreads();
+    // Z[j][s] -= sum_c v_{k0+c}[j] W2[c][s]  (j > k0 + c)
+    for (int j = k0 + 1 + rc; j < n; j += kNB) {
+      const int cmax = min(nb, j - k0);
+      double acc = 0.0;
+      for (int c = 0; c < cmax; ++c) acc = fma(vsb[(size_t)c * n + j], w2[c][sc], acc);
+      zs[j * kBtCols + sc] -= acc;
+    }
+    __syncthreads();
+  }
+  for (int t = tid; t < n * kBtCols; t += blockDim.x) {
+    const int j = t / kBtCols, c = c0 + t % kBtCols;
+    if (c < n) V0[(size_t)j * n + c] = zs[t];
+  }
+}
+
+// E_ij = S_ij / (S_jj - S_ii) (i != j), 0 on the diagonal; runs only when flags[2] (the first
+// orthogonality check failed); flags[1] = 1 when any |E_ij| > limit or is not finite
+__global__ void refine_e_kernel(const double *__restrict__ S, int n, int64_t stride, double limit,
+                                double *__restrict__ E, int *flags) {
+  const int prob = blockIdx.y;
+  if (flags[prob * 4 + 2] == 0) return;
+  const double *Sp = S + (size_t)prob * stride;
+  double *Ep = E + (size_t)prob * stride;
+  bool bad = false;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)n * n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(t / n), c = (int)(t % n);
+    double x = 0.0;
+    if (r != c) {
+      const double den = Sp[(size_t)c * n + c] - Sp[(size_t)r * n + r];
+      const double sij = Sp[t];
+      x = sij == 0.0 ? 0.0 : sij / den;
+      if (!(fabs(x) <= limit)) bad = true;
+    }
+    Ep[t] = x;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags + prob * 4 + 1, 1);
+}
+
+// after the E kernels of all blocks: zero E when any block flagged it (P + P F == P exactly)
+__global__ void refine_gate_kernel(double *__restrict__ E, int n, int64_t stride, const int *flags) {
+  const int prob = blockIdx.y;
+  if (flags[prob * 4 + 2] == 0 || flags[prob * 4 + 1] == 0) return;
+  double *Ep = E + (size_t)prob * stride;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)n * n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    Ep[t] = 0.0;
+}
+
+// dst <- src when the refinement did not run (flags[2] == 0)
+__global__ void copy_if_converged_kernel(const double *__restrict__ src, double *__restrict__ dst, int64_t count,
+                                         int64_t stride, const int *flags) {
+  const int prob = blockIdx.y;
+  if (flags[prob * 4 + 2] != 0) return;
+  const double *sp = src + (size_t)prob * stride;
+  double *dp = dst + (size_t)prob * stride;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x)
+    dp[t] = sp[t];
+}
+
+// orthogonality check: flags[slot] = 1 when some column pair of W' fails the reference's test
+// |apq| <= tol sqrt(app aqq) (_core.pyx:104) or anything is not finite; with gate_slot >= 0 it
+// runs only when flags[gate_slot] != 0
+__global__ void offrel_check_kernel(const double *__restrict__ S, int n, int64_t stride, double tol2, int *flags,
+                                    int slot, int gate_slot) {
+  const int prob = blockIdx.y;
+  if (gate_slot >= 0 && flags[prob * 4 + gate_slot] == 0) return;
+  const double *Sp = S + (size_t)prob * stride;
+  bool need = false;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)n * n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(t / n), c = (int)(t % n);
+    if (r == c) continue;
+    const double sij = Sp[t], sii = Sp[(size_t)r * n + r], sjj = Sp[(size_t)c * n + c];
+    if (!(sij * sij <= tol2 * (sii * sjj))) need = true;
+  }
+  if (__any_sync(0xffffffffu, need) && (threadIdx.x & 31) == 0) atomicOr(flags + prob * 4 + slot, 1);
+}
+
+// the Jacobi sweeps still run when the first check failed and the refined one failed too
+__global__ void jacobi_gate_kernel(const int *flags, int *gate, int batch) {
+  const int prob = blockIdx.x * blockDim.x + threadIdx.x;
+  if (prob < batch) gate[prob] = (flags[prob * 4 + 2] != 0 && flags[prob * 4 + 3] != 0) ? 1 : 0;
+}
+
+}  // namespace
+
+// ================================================================== host side
+struct EigPlan {
+  int C = 0, threads = 0, ldr = 0;
+  size_t smem = 0;
+  bool ok = false;
+  bool reg = false;  // register-resident sytrd_reg_kernel
+};
+
+constexpr int kSytrdMaxE = 18;  // n <= 576
+static void (*sytrd_pick(int n))(SytrdArgs) {
+  switch ((n + 31) / 32) {
+#define LRAMM_SYTRD_E(EE) \
+  case EE: return sytrd_cluster_kernel<EE>;
+    LRAMM_SYTRD_E(1) LRAMM_SYTRD_E(2) LRAMM_SYTRD_E(3) LRAMM_SYTRD_E(4) LRAMM_SYTRD_E(5) LRAMM_SYTRD_E(6)
+    LRAMM_SYTRD_E(7) LRAMM_SYTRD_E(8) LRAMM_SYTRD_E(9) LRAMM_SYTRD_E(10) LRAMM_SYTRD_E(11) LRAMM_SYTRD_E(12)
+    LRAMM_SYTRD_E(13) LRAMM_SYTRD_E(14) LRAMM_SYTRD_E(15) LRAMM_SYTRD_E(16) LRAMM_SYTRD_E(17) LRAMM_SYTRD_E(18)
+#undef LRAMM_SYTRD_E
+    default: return nullptr;
+  }
+}
+
+static void (*sytrd_reg_pick(int n))(SytrdArgs) {
+  switch ((n + 31) / 32) {
+#define LRAMM_SYTRD_R(EE) \
+  case EE: return sytrd_reg_kernel<EE>;
+    LRAMM_SYTRD_R(1) LRAMM_SYTRD_R(2) LRAMM_SYTRD_R(3) LRAMM_SYTRD_R(4) LRAMM_SYTRD_R(5) LRAMM_SYTRD_R(6)
+    LRAMM_SYTRD_R(7) LRAMM_SYTRD_R(8) LRAMM_SYTRD_R(9) LRAMM_SYTRD_R(10) LRAMM_SYTRD_R(11) LRAMM_SYTRD_R(12)
+#undef LRAMM_SYTRD_R
+    default: return nullptr;
+  }
+}
+
+static EigPlan plan_sytrd(int n, int batch) {
+  EigPlan p;
+  static const int env_reg = [] {
+    const char *s = getenv("LRAMM_EIG_REG");
+    return s ? atoi(s) : 1;
+  }();
+  static const int env_c0 = [] {
+    const char *s = getenv("LRAMM_EIG_CLUSTER");
+    return s ? atoi(s) : 0;
+  }();
+  if (env_reg && n <= 32 * kSytrdRegMaxE) {
+    const int E = (n + 31) / 32, rm = sytrd_rmax(E), nrw = 7;
+    p.ldr = (int)round_up(n, 2) + 1;
+    int pick = 0;
+    auto rows_per_warp = [&](int C) { return (int)ceil_div(ceil_div(n, C), nrw); };
+    if (env_c0 > 0 && rows_per_warp(env_c0) <= rm) pick = env_c0;
+    if (!pick && batch >= 16)
+      for (int C : {1, 2, 4, 8, 16})
+        if (rows_per_warp(C) <= rm) {
+          pick = C;
+          break;
+        }
+    if (!pick)
+      for (int C : {1, 2, 4, 8, 16})
+        if (rows_per_warp(C) <= std::min(rm, 3)) {
+          pick = C;
+          break;
+        }
+    if (!pick)
+      for (int C : {1, 2, 4, 8, 16})
+        if (rows_per_warp(C) <= rm) {
+          pick = C;
+          break;
+        }
+    if (pick) {
+      p.C = pick;
+      p.threads = 256;
+      p.smem = (size_t)(4 * ceil_div(n, pick) + 4 * p.ldr) * sizeof(double);
+      p.ok = p.reg = true;
+      return p;
+    }
+  }
+  int optin = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t budget = (size_t)optin - 2048;
+  p.ldr = (int)round_up(n, 2) + 1;  // odd stride: column-strided lane accesses spread banks
+  auto smem_for = [&](int C) {
+    const int nlmax = (int)ceil_div(n, C);
+    return (size_t)((size_t)nlmax * p.ldr + 4 * nlmax + 4 * p.ldr) * sizeof(double);
+  };
+  static const int env_c = [] {
+    const char *s = getenv("LRAMM_EIG_CLUSTER");
+    return s ? atoi(s) : 0;
+  }();
+  int pick = 0;
+  if (env_c > 0 && smem_for(env_c) <= budget) pick = env_c;
+  if (!pick && batch >= 16 && smem_for(1) <= budget) pick = 1;  // batched: one CTA per problem
+  if (!pick)
+    for (int C : {1, 2, 4, 8, 16})
+      if (smem_for(C) <= budget && ceil_div(n, C) <= 24) {
+        pick = C;
+        break;
+      }
+  if (!pick)
+    for (int C : {16, 8})
+      if (smem_for(C) <= budget) {
+        pick = C;
+        break;
+      }
+  if (!pick || n > 32 * kSytrdMaxE) return p;
+  p.C = pick;
+  p.smem = smem_for(pick);
+  const int rows = (int)ceil_div(n, pick);
+  int warps = std::min(20, std::max(8, rows + 1));  // warp 0 + one warp per row where possible
+  static const int env_w = [] {
+    const char *s = getenv("LRAMM_EIG_WARPS");
+    return s ? atoi(s) : 0;
+  }();
+  if (env_w > 0) warps = std::min(20, std::max(2, env_w));
+  p.threads = 32 * warps;
+  p.ok = true;
+  return p;
+}
+
+static size_t twisted_smem(int n, int tpb) { return (size_t)(2 * n + 2 * (size_t)n * tpb) * sizeof(double); }
+static int twisted_threads(int n) {
+  int t = 32;
+  while (t > 1 && twisted_smem(n, t) > 200 * 1024) t >>= 1;
+  return t;
+}
+
+// whether the preconditioner runs for an n x n Jacobi (LRAMM_EIG_PRE = 0 / 1 overrides)
+bool eig_precondition_enabled(int n, int batch) {
+  static const int env = [] {
+    const char *s = getenv("LRAMM_EIG_PRE");
+    return s ? atoi(s) : -1;
+  }();
+  if (env == 0) return false;
+  if (n < 3) return false;
+  if (env != 1 && n < 48) return false;
+  return plan_sytrd(n, batch).ok;
+}
+
+struct EigWs {
+  double *Rt, *G, *V, *Z, *D, *Zo, *V0, *P, *S, *E, *P2, *d, *e, *tau, *lam, *T, *gemm;
+  int *flags;
+  size_t gemm_bytes;
+};
+static EigWs carve_eig(Arena &ar, int n, int batch) {
+  EigWs w;
+  const int64_t nn = (int64_t)n * n * batch;
+  w.Rt = ar.take<double>(nn);
+  w.G = ar.take<double>(nn);
+  w.V = ar.take<double>(nn);
+  w.Z = ar.take<double>(nn);
+  w.D = ar.take<double>(nn);
+  w.Zo = ar.take<double>(nn);
+  w.V0 = ar.take<double>(nn);
+  w.P = ar.take<double>(nn);
+  w.S = ar.take<double>(nn);
+  w.E = ar.take<double>(nn);
+  w.P2 = ar.take<double>(nn);
+  w.d = ar.take<double>((int64_t)n * batch);
+  w.e = ar.take<double>((int64_t)n * batch);
+  w.tau = ar.take<double>((int64_t)n * batch);
+  w.lam = ar.take<double>((int64_t)n * batch);
+  w.T = ar.take<double>(ceil_div(n - 2, kNB) * kNB * kNB * batch);
+  w.flags = ar.take<int>(4 * batch);
+  w.gemm_bytes = std::max(dgemm_ws_bytes(1, n, n, n), dgemm_ws_bytes(0, n, n, n));
+  w.gemm = ar.take<double>((int64_t)(w.gemm_bytes / 8 + 1));
+  return w;
+}
+
+size_t eig_precondition_ws_bytes(int n, int batch) {
+  Arena ar;
+  ar.dry = true;
+  carve_eig(ar, n, batch);
+  return ar.off + 256;
+}
+
+// R: n x n row-major (the Jacobi operand W = R^T, column-major), one problem (batch == 1).
+// On return R holds R' = (W V0)^T (or R unchanged when the preconditioner failed) and
+// *jac_gate (device int) is nonzero when the Jacobi sweeps still have to run.
+int eig_precondition_device(double *R, int n, int *jac_gate, void *ws, size_t ws_bytes, cudaStream_t st) {
+  const int batch = 1;
+  EigPlan p = plan_sytrd(n, batch);
+  if (!p.ok) return fail(LRAMM_ERR_UNSUPPORTED, "eig preconditioner: n = %d does not fit", n);
+  Arena ar(ws, ws_bytes);
+  EigWs w = carve_eig(ar, n, batch);
+  if (!ar.ok()) return fail(LRAMM_ERR_WORKSPACE, "eig preconditioner: workspace too small");
+  LRAMM_CUDA_TRY(cudaMemsetAsync(w.flags, 0, 4 * sizeof(int) * batch, st));
+  LRAMM_CUDA_TRY(cudaMemsetAsync(w.V, 0, (size_t)n * n * sizeof(double) * batch, st));
+  // G = R R^T = Rt^T Rt
+  LRAMM_TRY(transpose_device(R, n, n, n, w.Rt, n, st));
+  DgemmOptions sym;
+  sym.sym = 1;
+  LRAMM_TRY(dgemm_device_ex(1, n, n, n, w.Rt, n, w.Rt, n, w.G, n, w.gemm, w.gemm_bytes, st, sym));
+  // tridiagonalisation
+  {
+    void (*kern)(SytrdArgs) = p.reg ? sytrd_reg_pick(n) : sytrd_pick(n);
+    if (!kern) return fail(LRAMM_ERR_UNSUPPORTED, "eig preconditioner: n = %d too wide", n);
+    static PerDeviceOnce once;
+    LRAMM_CUDA_TRY(once.run([] {
+      cudaError_t e = cudaSuccess;
+      for (int E = 1; E <= kSytrdMaxE && e == cudaSuccess; ++E) {
+        void (*k)(SytrdArgs) = sytrd_pick(32 * E);
+        e = allow_max_dyn_smem(k);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      }
+      for (int E = 1; E <= kSytrdRegMaxE && e == cudaSuccess; ++E) {
+        void (*k)(SytrdArgs) = sytrd_reg_pick(32 * E);
+        e = allow_max_dyn_smem(k);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      }
+      if (e == cudaSuccess) e = allow_max_dyn_smem(backtransform_kernel);
+      if (e == cudaSuccess) e = allow_max_dyn_smem(reflector_t_kernel);
+      if (e == cudaSuccess) e = allow_max_dyn_smem(tridiag_twisted_kernel);
+      return e;
+    }));
+    SytrdArgs a;
+    a.G = w.G;
+    a.ldg = n;
+    a.g_stride = (int64_t)n * n;
+    a.n = n;
+    a.d = w.d;
+    a.e = w.e;
+    a.tau = w.tau;
+    a.V = w.V;
+    a.ldr = p.ldr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(p.C * batch));
+    cfg.blockDim = dim3((unsigned)p.threads);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)p.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LRAMM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a));
+  }
+  // eigenvalues, eigenvectors of T
+  {
+    const int wpb = 2;  // spread the eigenvalue warps over the SMs
+    tridiag_bisect_kernel<<<dim3((unsigned)ceil_div(n, wpb), batch), 32 * wpb, (size_t)2 * n * sizeof(double), st>>>(
+        w.d, w.e, n, w.lam);
+    LRAMM_LAUNCH_CHECK();
+    const int tpb = twisted_threads(n);
+    tridiag_twisted_kernel<<<dim3((unsigned)ceil_div(n, tpb), batch), tpb, twisted_smem(n, tpb), st>>>(w.d, w.e, n,
+                                                                                                  w.lam, w.Z);
+    LRAMM_LAUNCH_CHECK();
+  }
+  const unsigned eblocks = (unsigned)std::min<int64_t>(ceil_div((int64_t)n * n, 256), 4LL * num_sms());
+  // Lowdin: D = Z^T Z - I; Zo = Z - Z D / 2; a defect above 1e-4 (clustered eigenvalues) means
+  // the preconditioner failed -> identity (Jacobi on the untouched W)
+  LRAMM_TRY(dgemm_device_ex(1, n, n, n, w.Z, n, w.Z, n, w.D, n, w.gemm, w.gemm_bytes, st, sym));
+  eig_defect_kernel<<<dim3(eblocks, batch), 256, 0, st>>>(w.D, n, (int64_t)n * n, 1e-4, w.flags);
+  LRAMM_LAUNCH_CHECK();
+  {
+    DgemmOptions lo;
+    lo.alpha = -0.5;
+    lo.beta = 1.0;
+    lo.cin = w.Z;
+    lo.ldci = n;
+    LRAMM_TRY(dgemm_device_ex(0, n, n, n, w.Z, n, w.D, n, w.Zo, n, w.gemm, w.gemm_bytes, st, lo));
+  }
+  {
+    const int nblk = (int)ceil_div(n - 2, kNB);
+    reflector_t_kernel<<<dim3((unsigned)nblk, batch), 256, (size_t)kNB * n * sizeof(double), st>>>(w.V, w.tau, n, w.T);
+    LRAMM_LAUNCH_CHECK();
+    backtransform_kernel<<<dim3((unsigned)ceil_div(n, kBtCols), batch), 256, (size_t)n * (kBtCols + kNB) * sizeof(double), st>>>(
+        w.Zo, w.V, w.T, n, w.flags, w.V0);
+    LRAMM_LAUNCH_CHECK();
+  }
+  // P = W V0 = Rt V0 (row-major P == W' as a plain matrix); check; one-sided refinement only
+  // when the check failed: P2 = P + P F, F = E + E^2 / 2 (orthogonal to O(|E|^3))
+  LRAMM_TRY(dgemm_device_ex(0, n, n, n, w.Rt, n, w.V0, n, w.P, n, w.gemm, w.gemm_bytes, st, DgemmOptions{}));
+  LRAMM_TRY(dgemm_device_ex(1, n, n, n, w.P, n, w.P, n, w.S, n, w.gemm, w.gemm_bytes, st, sym));
+  offrel_check_kernel<<<dim3(eblocks, batch), 256, 0, st>>>(w.S, n, (int64_t)n * n, 1e-26, w.flags, 2, -1);
+  LRAMM_LAUNCH_CHECK();
+  refine_e_kernel<<<dim3(eblocks, batch), 256, 0, st>>>(w.S, n, (int64_t)n * n, 1e-4, w.E, w.flags);
+  LRAMM_LAUNCH_CHECK();
+  refine_gate_kernel<<<dim3(eblocks, batch), 256, 0, st>>>(w.E, n, (int64_t)n * n, w.flags);
+  LRAMM_LAUNCH_CHECK();
+  {
+    DgemmOptions f;  // F = E + E E / 2   (into D: free after the Lowdin step)
+    f.alpha = 0.5;
+    f.beta = 1.0;
+    f.cin = w.E;
+    f.ldci = n;
+    f.gate = w.flags + 2;
+    f.gate_run_if_nonzero = 1;
+    LRAMM_TRY(dgemm_device_ex(0, n, n, n, w.E, n, w.E, n, w.D, n, w.gemm, w.gemm_bytes, st, f));
+    DgemmOptions rf;  // P2 = P + P F
+    rf.alpha = 1.0;
+    rf.beta = 1.0;
+    rf.cin = w.P;
+    rf.ldci = n;
+    rf.gate = w.flags + 2;
+    rf.gate_run_if_nonzero = 1;
+    LRAMM_TRY(dgemm_device_ex(0, n, n, n, w.P, n, w.D, n, w.P2, n, w.gemm, w.gemm_bytes, st, rf));
+    copy_if_converged_kernel<<<dim3(eblocks, batch), 256, 0, st>>>(w.P, w.P2, (int64_t)n * n, (int64_t)n * n, w.flags);
+    LRAMM_LAUNCH_CHECK();
+    DgemmOptions s2 = sym;
+    s2.gate = w.flags + 2;
+    s2.gate_run_if_nonzero = 1;
+    LRAMM_TRY(dgemm_device_ex(1, n, n, n, w.P2, n, w.P2, n, w.S, n, w.gemm, w.gemm_bytes, st, s2));
+  }
+  offrel_check_kernel<<<dim3(eblocks, batch), 256, 0, st>>>(w.S, n, (int64_t)n * n, 1e-26, w.flags, 3, 2);
+  LRAMM_LAUNCH_CHECK();
+  // R' = P2^T (the Jacobi operand, column-major W')
+  LRAMM_TRY(transpose_device(w.P2, n, n, n, R, n, st));
+  jacobi_gate_kernel<<<1, 32, 0, st>>>(w.flags, jac_gate, batch);
+  LRAMM_LAUNCH_CHECK();
+  return LRAMM_OK;
+}
+
+}  // namespace lramm
