@@ -53,6 +53,16 @@ using sm100::cp_async8;
 using sm100::cp_async_wait_all;
 namespace {
 
+// 1/x to ~1 ulp: MUFU reciprocal seed + two Newton steps (x normal, |x| >= pivmin)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // ------------------------------------------------------------------ CTA reductions
 template <int NW>
 __device__ __forceinline__ double cta_sum(double v, double *red) {
@@ -344,17 +354,64 @@ __global__ void __launch_bounds__(640, 1) sytrd_cluster_kernel(SytrdArgs a) {
   cl.sync();  // peers may still be reading this CTA's shared memory
 }
 
-// Register-resident variant (n <= 32 * kSytrdRegMaxE): each row warp keeps up to RMAX rows of
-// the CTA in registers (lane owns columns lane + 32 e), so a step touches shared memory only
-// for the gathered vectors.  Warp 0 derives the reflector (as above); warps 1.. update their
-// rows (inactive columns carry p = v = 0, so the rank-2 update leaves them unchanged) and form
-// the next dot products from registers.
-constexpr int kSytrdRegMaxE = 12;
-__host__ __device__ constexpr int sytrd_rmax(int e) { return 96 / e - 2 > 24 ? 24 : 96 / e - 2; }
+// Push variant: no cluster barrier and no gather per step.  Each CTA pushes (p_i, A[i, k+2]) of
+// its rows into every CTA's receive buffer with st.async, whose bytes complete a transaction
+// count on the receiver's mbarrier (one per buffer parity); a CTA starts step k as soon as all
+// rows of that step have landed.  RM > 0: each row warp keeps up to RM rows in registers (lane
+// owns columns lane + 32 e); RM == 0: rows stay in shared memory and the update is fused with
+// the next dot products after the reflector is known.
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, double a, double b, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "d"(a), "d"(b), "r"(rbar)
+               : "memory");
+}
 
-template <int E>
-__global__ void __launch_bounds__(256, 1) sytrd_reg_kernel(SytrdArgs a) {
-  constexpr int RM = sytrd_rmax(E);
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double a, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(a),
+               "r"(rbar)
+               : "memory");
+}
+
+// dlarfg without division or square root on the chain: rs = 1/sqrt(alpha^2 + s2) (MUFU seed +
+// third-order correction), beta = -sign(alpha)/rs, tau = 1 + |alpha| rs, 1/(alpha - beta) =
+// sign(alpha) / (|alpha| + 1/rs); tiny operands take the exact library path
+__device__ __forceinline__ void householder_fast(double alpha, double s2, double &beta, double &tau, double &scl) {
+  const double t = fma(alpha, alpha, s2);
+  if (s2 == 0.0) {
+    tau = 0.0;
+    beta = alpha;
+    scl = 0.0;
+    return;
+  }
+  if (!(t >= 0x1p-900 && t <= 0x1p900)) {
+    householder(alpha, s2, beta, tau, scl);
+    return;
+  }
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(t));
+  const double e = fma(-(y * y), t, 1.0);
+  const double rs = fma(fma(e, 0.375, 0.5), y * e, y);
+  const double nrm = t * rs;
+  const double aa = fabs(alpha);
+  beta = -copysign(nrm, alpha);
+  tau = fma(aa, rs, 1.0);
+  scl = copysign(rcp_nr(aa + nrm), alpha);
+}
+
+constexpr int kSytrdRegMaxE = 12;
+
+template <int E, int RM>
+__global__ void __launch_bounds__(256, 1) sytrd_push_kernel(SytrdArgs a) {
+  constexpr int RR = RM > 0 ? RM : 1;
   cg::cluster_group cl = cg::this_cluster();
   const int C = (int)cl.num_blocks();  // a power of two
   const int lgC = __ffs(C) - 1;
@@ -362,41 +419,60 @@ __global__ void __launch_bounds__(256, 1) sytrd_reg_kernel(SytrdArgs a) {
   const int prob = blockIdx.x >> lgC;
   const int n = a.n, ldr = a.ldr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5, nth = blockDim.x;
-  const int nrw = nwarp - 1;                 // row warps
-  const int nl = (n - me + C - 1) >> lgC;   // local rows: global i = me + li * C
-  const int nlmax = (n + C - 1) >> lgC;
+  // row warps: all but warp 0 (the reflector) and warp 4, which shares warp 0's SM sub-partition
+  // (its fp64 pipe) -- the reflector chain is the critical path of a step
+  const int nrw = nwarp - 2;
+  const int rwi = warp == 0 || warp == 4 ? -1 : (warp < 4 ? warp - 1 : warp - 2);
+  const int nl = (n - me + C - 1) >> lgC;  // local rows: global i = me + li * C
   extern __shared__ __align__(16) double sm[];
-  double2 *pub = reinterpret_cast<double2 *>(sm);  // [2][nlmax] (p_i, a_{i,k+1})
-  double *pf = sm + 4 * nlmax;                     // [ldr] gathered p
-  double *rk = pf + ldr;                           // [ldr] gathered column k+1 (= row k+1)
-  double *vb = rk + ldr;                           // [2][ldr] reflectors (current / next)
+  double2 *rbuf = reinterpret_cast<double2 *>(sm);  // [2][n] received (p_j, A[j, k+1])
+  double *sbuf = sm + 4 * (size_t)n;                // [2][16] received partials of s = p . v
+  double2 *stage = reinterpret_cast<double2 *>(sbuf + 32);  // [nlmax] pushes staged behind a barrier
+  double2 *pf0 = stage;
+  double *vb = sbuf + 32 + 2 * ((n + C - 1) >> lgC);  // [2][ldr]
+  double *rk = vb + 2 * (size_t)ldr;                // [ldr] row 0 at start
+  double *A = rk + ldr;                             // RM == 0: [nl][ldr]
   __shared__ double red[2][32];
+  __shared__ double wpart[8];
   __shared__ double hh[4];
+  __shared__ __align__(8) uint64_t bars[2];
 
   const double *G = a.G + (size_t)prob * a.g_stride;
   double *dout = a.d + (size_t)prob * n, *eout = a.e + (size_t)prob * n, *tout = a.tau + (size_t)prob * n;
   double *Vout = a.V + (size_t)prob * n * n;
 
+  if (tid == 0) {
+    sm100::mbar_init(&bars[0], 1);
+    sm100::mbar_init(&bars[1], 1);
+    sm100::fence_barrier_init();
+  }
   double dm = 0.0;
   for (int i = tid; i < n; i += nth) dm = fmax(dm, fabs(G[(int64_t)i * a.ldg + i]));
   dm = cta_max(dm, red[0]);
   double scale = 1.0;
   if (dm > 0.0 && dm <= DBL_MAX) scale = ldexp(1.0, -2 * (ilogb(dm) >> 1));
-  // rows of this warp: li = (warp - 1) + r * nrw
-  double x[RM][E];
-  int gi[RM];
+  double x[RR][E];
+  int gi[RR];
+  if (RM > 0) {
 #pragma unroll
-  for (int r = 0; r < RM; ++r) {
-    const int li = warp - 1 + r * nrw;
-    gi[r] = (warp >= 1 && li < nl) ? me + (li << lgC) : -1;
-    const double *src = G + (int64_t)(gi[r] < 0 ? 0 : gi[r]) * a.ldg;
+    for (int r = 0; r < RR; ++r) {
+      const int li = rwi + r * nrw;
+      gi[r] = (rwi >= 0 && li < nl) ? me + (li << lgC) : -1;
+      const double *src = G + (int64_t)(gi[r] < 0 ? 0 : gi[r]) * a.ldg;
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int j = lane + 32 * e;
-      x[r][e] = (gi[r] >= 0 && j < n) ? src[j] * scale : 0.0;
+      for (int e = 0; e < E; ++e) {
+        const int j = lane + 32 * e;
+        x[r][e] = (gi[r] >= 0 && j < n) ? src[j] * scale : 0.0;
+      }
+    }
+  } else {
+    for (int li = warp; li < nl; li += nwarp) {
+      const double *src = G + (int64_t)(me + (li << lgC)) * a.ldg;
+      for (int j = lane; j < n; j += 32) A[(size_t)li * ldr + j] = src[j] * scale;
     }
   }
   for (int j = tid; j < n; j += nth) rk[j] = G[j] * scale;
+  for (int j = tid; j < 32; j += nth) sbuf[j] = 0.0;
   __syncthreads();
   double *v = vb, *vn = vb + ldr;
   double tau;
@@ -417,7 +493,18 @@ __global__ void __launch_bounds__(256, 1) sytrd_reg_kernel(SytrdArgs a) {
       tout[0] = tau;
     }
   }
-  __syncthreads();
+  const uint32_t rbuf_s = sm100::smem_u32(rbuf), bar_s = sm100::smem_u32(bars);
+  cl.sync();  // barriers initialised everywhere before any remote push
+  if (tid == 0) sm100::mbar_arrive_expect_tx(&bars[0], 16u * (uint32_t)(n - 1));
+  // push (p_i, A[i, j]) of local row i to every CTA's receive buffer (parity bp)
+  auto push = [&](int i, double pv, double cv, int bp) {
+    if (lane < C) {
+      const uint32_t ra = mapa_u32(rbuf_s + (uint32_t)(bp * n + i) * 16u, lane);
+      const uint32_t rb = mapa_u32(bar_s + (uint32_t)bp * 8u, lane);
+      st_async_v2(ra, pv, cv, rb);
+    }
+  };
+
   {  // p_0 and the column-1 entries of own rows i >= 1
     double vv[E];
 #pragma unroll
@@ -425,37 +512,37 @@ __global__ void __launch_bounds__(256, 1) sytrd_reg_kernel(SytrdArgs a) {
       const int j = lane + 32 * e;
       vv[e] = j < n ? v[j] : 0.0;
     }
-#pragma unroll
-    for (int r = 0; r < RM; ++r) {
+    // prologue runs once: dots staged, barrier, then pushes
+    for (int li = warp; li < nl; li += nwarp) {
+      const int i = me + (li << lgC);
+      if (i < 1) continue;
       double dot = 0.0;
-#pragma unroll
-      for (int e = 0; e < E; ++e) dot = fma(x[r][e], vv[e], dot);
+      for (int j = lane; j < n; j += 32) dot = fma(G[(int64_t)i * a.ldg + j] * scale, v[j], dot);
       dot = warp_allsum(dot);
-      const double c1 = __shfl_sync(0xffffffffu, x[r][0], 1);
-      if (gi[r] >= 1 && lane == 0) pub[(gi[r] >> lgC)] = make_double2(tau * dot, c1);
+      if (lane == 0) pf0[li] = make_double2(tau * dot, G[(int64_t)i * a.ldg + 1] * scale);
+    }
+    __syncthreads();
+    for (int li = warp; li < nl; li += nwarp) {
+      const int i = me + (li << lgC);
+      if (i >= 1) push(i, pf0[li].x, pf0[li].y, 0);
     }
   }
-  const uint32_t pub_s = sm100::smem_u32(pub);
-  cl.sync();
 
   for (int k = 0; k <= n - 3; ++k) {
     const int par = k & 1, npar = par ^ 1;
     const bool last = (k == n - 3);
-    for (int j = k + 1 + tid; j < n; j += nth) {
-      const uint32_t pa = mapa_u32(pub_s + (par * nlmax + (j >> lgC)) * 16, j & (C - 1));
-      double pj, cj;
-      asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(pj), "=d"(cj) : "r"(pa) : "memory");
-      pf[j] = pj;
-      rk[j] = cj;
-    }
-    __syncthreads();
-    // w_j = p_j - c v_j on this lane's columns (zero for j <= k)
+    STR_MARK(t0);
+    mbar_wait_acq_cluster(bar_s + par * 8, (uint32_t)((k >> 1) & 1));
+    if (tid == 0 && !last) sm100::mbar_arrive_expect_tx(&bars[npar], 16u * (uint32_t)(n - k - 2));
+    STR_MARK(t1);
+    const double2 *rb = rbuf + (size_t)par * n;
+    // s = p . v from the CTAs' partials (fixed order); w_j = p_j - c v_j on this lane's columns
     double wr[E], vr[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int j = lane + 32 * e;
       const bool in = j > k && j < n;
-      wr[e] = in ? pf[j] : 0.0;
+      wr[e] = in ? rb[j].x : 0.0;
       vr[e] = in ? v[j] : 0.0;
     }
     double sacc = 0.0;
@@ -464,19 +551,22 @@ __global__ void __launch_bounds__(256, 1) sytrd_reg_kernel(SytrdArgs a) {
     const double c = 0.5 * tau * warp_allsum(sacc);
 #pragma unroll
     for (int e = 0; e < E; ++e) wr[e] = fma(-c, vr[e], wr[e]);
+    STR_MARK(t2);
     if (warp == 0) {
-      // ---- column k+1 of A_{k+1}: r_j = A_k[j,k+1] - v_j w_{k+1} - w_j (v_{k+1} = 1)
-      const double wk1 = pf[k + 1] - c;
+      // column k+1 of A_{k+1}: r_j = A_k[j, k+1] - v_j w_{k+1} - w_j   (v_{k+1} = 1)
+      STR_MARK(h0);
+      const double wk1 = rb[k + 1].x - c;
       double rr[E];
       double s2 = 0.0;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int j = lane + 32 * e;
-        rr[e] = (j > k && j < n) ? rk[j] - wr[e] - wk1 * vr[e] : 0.0;
+        rr[e] = (j > k && j < n) ? rb[j].y - wr[e] - wk1 * vr[e] : 0.0;
         if (j >= k + 3) s2 = fma(rr[e], rr[e], s2);
       }
+      STR_MARK(h1);
       s2 = warp_allsum(s2);
-      // alpha = r_{k+2}, d_{k+1} = r_{k+1}: from the owning lanes
+      STR_MARK(h2);
       double al = 0.0, dk = 0.0;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
@@ -485,83 +575,122 @@ __global__ void __launch_bounds__(256, 1) sytrd_reg_kernel(SytrdArgs a) {
       }
       const double alpha = __shfl_sync(0xffffffffu, al, (k + 2) & 31);
       const double dk1 = __shfl_sync(0xffffffffu, dk, (k + 1) & 31);
+      STR_MARK(h3);
       if (!last) {
         double beta, tn, scl;
-        householder(alpha, s2, beta, tn, scl);
-        double *vrow = Vout + (size_t)(k + 1) * n;
+        householder_fast(alpha, s2, beta, tn, scl);
+        STR_MARK(h4);
+        STR_ADD(12, h4, h4);
+        STR_ADD(8, h0, h1);
+        STR_ADD(9, h1, h2);
+        STR_ADD(10, h2, h3);
+        STR_ADD(11, h3, h4);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const int j = lane + 32 * e;
-          if (j < n) {
-            const double vj = j < k + 2 ? 0.0 : (j == k + 2 ? 1.0 : rr[e] * scl);
-            vn[j] = vj;
-            if (me == 0 && j >= k + 2) vrow[j] = vj;
-          }
+          if (j < n) vn[j] = j < k + 2 ? 0.0 : (j == k + 2 ? 1.0 : rr[e] * scl);
         }
         if (lane == 0) {
           hh[0] = tn;
-          if (me == 0) {
-            dout[k + 1] = dk1;
-            eout[k + 1] = beta;
-            tout[k + 1] = tn;
-          }
+          hh[1] = dk1;
+          hh[2] = beta;
         }
       } else if (me == 0 && lane == 0) {
         dout[n - 2] = dk1;
         eout[n - 2] = alpha;
       }
-    } else {
-      // ---- own rows i >= k+2 in registers: A -= v w^T + w v^T
+    } else if (RM > 0) {
+      // own rows i >= k+2 in registers: A -= v w^T + w v^T
 #pragma unroll
-      for (int r = 0; r < RM; ++r) {
+      for (int r = 0; r < RR; ++r) {
         if (gi[r] >= k + 2) {
-          const double vi = v[gi[r]], wi = pf[gi[r]] - c * vi;
+          const double vi = v[gi[r]], wi = rb[gi[r]].x - c * vi;
 #pragma unroll
           for (int e = 0; e < E; ++e) x[r][e] = fma(-wi, vr[e], fma(-vi, wr[e], x[r][e]));
         }
       }
       if (last) {
 #pragma unroll
-        for (int r = 0; r < RM; ++r)
+        for (int r = 0; r < RR; ++r)
           if (gi[r] == n - 1) {
 #pragma unroll
             for (int e = 0; e < E; ++e)
               if (lane + 32 * e == n - 1) dout[n - 1] = x[r][e];
           }
       }
+    } else if (last && warp == 1 && lane == 0 && ((n - 1) & (C - 1)) == me) {
+      // a_{n-1,n-1} - 2 v_{n-1} w_{n-1}
+      const double vl = v[n - 1], wl = rb[n - 1].x - c * vl;
+      dout[n - 1] = A[(size_t)((n - 1) >> lgC) * ldr + n - 1] - 2.0 * vl * wl;
     }
     if (last) break;
+    STR_MARK(t3);
     __syncthreads();
-    // ---- p_{k+1} and the column-(k+2) entry of own rows i >= k+2
+    STR_MARK(t4);
+    // ---- p_{k+1} and the column-(k+2) entry of own rows i >= k+2, pushed to every CTA
     const double tn = hh[0];
-    if (warp >= 1) {
-      double vv[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int j = lane + 32 * e;
-        vv[e] = j < n ? vn[j] : 0.0;  // zero below k+2 by construction
+    if (warp == 4 && me == 0) {  // outputs, off the reflector chain
+      double *vrow = Vout + (size_t)(k + 1) * n;
+      for (int j = k + 2 + lane; j < n; j += 32) vrow[j] = vn[j];
+      if (lane == 0) {
+        dout[k + 1] = hh[1];
+        eout[k + 1] = hh[2];
+        tout[k + 1] = tn;
       }
-      double dots[RM], cols[RM];
+    }
+    double vv[E];
 #pragma unroll
-      for (int r = 0; r < RM; ++r) {
+    for (int e = 0; e < E; ++e) {
+      const int j = lane + 32 * e;
+      vv[e] = j < n ? vn[j] : 0.0;  // zero below k+2 by construction
+    }
+    const int ek2 = (k + 2) >> 5, lk2 = (k + 2) & 31;
+    if (RM > 0) {
+      if (rwi >= 0) {
+        double dots[RR], cols[RR];
+#pragma unroll
+        for (int r = 0; r < RR; ++r) {
+          double dot = 0.0, ce = 0.0;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            dot = fma(x[r][e], vv[e], dot);
+            if (e == ek2) ce = x[r][e];
+          }
+          dots[r] = dot;
+          cols[r] = ce;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+          for (int r = 0; r < RR; ++r) dots[r] += __shfl_xor_sync(0xffffffffu, dots[r], o);
+        }
+#pragma unroll
+        for (int r = 0; r < RR; ++r) {
+          const double ck2 = __shfl_sync(0xffffffffu, cols[r], lk2);
+          if (gi[r] >= k + 2) push(gi[r], tn * dots[r], ck2, npar);
+        }
+      }
+    } else {
+      int li0 = (k + 2 - me + C - 1) >> lgC;
+      if (li0 < 0) li0 = 0;
+      for (int li = li0 + warp; li < nl; li += nwarp) {
+        const int i = me + (li << lgC);
+        double *ar = A + (size_t)li * ldr;
+        const double vi = v[i], wi = rb[i].x - c * vi;
         double dot = 0.0, ce = 0.0;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          dot = fma(x[r][e], vv[e], dot);
-          if (e == ((k + 2) >> 5)) ce = x[r][e];
+          const int j = lane + 32 * e;
+          if (j > k && j < n) {
+            const double xv = fma(-wi, vr[e], fma(-vi, wr[e], ar[j]));
+            ar[j] = xv;
+            dot = fma(xv, vv[e], dot);
+            if (e == ek2) ce = xv;
+          }
         }
-        dots[r] = dot;
-        cols[r] = ce;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-        for (int r = 0; r < RM; ++r) dots[r] += __shfl_xor_sync(0xffffffffu, dots[r], o);
-      }
-#pragma unroll
-      for (int r = 0; r < RM; ++r) {
-        const double ck2 = __shfl_sync(0xffffffffu, cols[r], (k + 2) & 31);
-        if (gi[r] >= k + 2 && lane == 0) pub[npar * nlmax + (gi[r] >> lgC)] = make_double2(tn * dots[r], ck2);
+        dot = warp_allsum(dot);
+        const double ck2 = __shfl_sync(0xffffffffu, ce, lk2);
+        push(i, tn * dot, ck2, npar);
       }
     }
     tau = tn;
@@ -570,9 +699,15 @@ __global__ void __launch_bounds__(256, 1) sytrd_reg_kernel(SytrdArgs a) {
       v = vn;
       vn = t;
     }
-    cl.sync();
+    STR_MARK(t5);
+    STR_ADD(0, t0, t1);
+    STR_ADD(1, t1, t2);
+    STR_ADD(2, t2, t3);
+    STR_ADD(3, t3, t4);
+    STR_ADD(4, t4, t5);
+    STR_ADD(6, t0, t5);
   }
-  cl.sync();  // peers may still be reading this CTA's shared memory
+  cl.sync();  // no CTA leaves while peers may still push into it
 }
 
 // ------------------------------------------------------------------ eigenvalues of T
@@ -663,16 +798,6 @@ __global__ void __launch_bounds__(256) tridiag_bisect_kernel(const double *__res
 }
 
 // ------------------------------------------------------------------ eigenvectors of T
-// 1/x to ~1 ulp: MUFU reciprocal seed + two Newton steps (x normal, |x| >= pivmin)
-__device__ __forceinline__ double rcp_nr(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
-
 // One thread per eigenvalue: stationary (L+ D+ L+^T) and progressive (U- D- U-^T) factorisations
 // of T - lambda I, twist index r = argmin |gamma_r|, gamma_r = D+_r + D-_r - (d_r - lambda);
 // z_r = 1, z_j = -L+_j z_{j+1} (j < r), z_{j+1} = -U-_{j+1} z_j (j >= r); normalised.
@@ -974,7 +1099,8 @@ struct EigPlan {
   int C = 0, threads = 0, ldr = 0;
   size_t smem = 0;
   bool ok = false;
-  bool reg = false;  // register-resident sytrd_reg_kernel
+  bool reg = false;  // st.async push variant (sytrd_push_kernel)
+  int rm = 0;
 };
 
 constexpr int kSytrdMaxE = 18;  // n <= 576
@@ -990,15 +1116,18 @@ static void (*sytrd_pick(int n))(SytrdArgs) {
   }
 }
 
-static void (*sytrd_reg_pick(int n))(SytrdArgs) {
-  switch ((n + 31) / 32) {
-#define LRAMM_SYTRD_R(EE) \
-  case EE: return sytrd_reg_kernel<EE>;
-    LRAMM_SYTRD_R(1) LRAMM_SYTRD_R(2) LRAMM_SYTRD_R(3) LRAMM_SYTRD_R(4) LRAMM_SYTRD_R(5) LRAMM_SYTRD_R(6)
-    LRAMM_SYTRD_R(7) LRAMM_SYTRD_R(8) LRAMM_SYTRD_R(9) LRAMM_SYTRD_R(10) LRAMM_SYTRD_R(11) LRAMM_SYTRD_R(12)
-#undef LRAMM_SYTRD_R
-    default: return nullptr;
-  }
+// sytrd_push_kernel<E, RM>: RM rows per row warp in registers (0: rows in shared memory)
+static void (*sytrd_push_pick(int n, int rm))(SytrdArgs) {
+  const int E = (n + 31) / 32;
+#define LRAMM_SP(EE, RR) \
+  if (E == EE && rm == RR) return sytrd_push_kernel<EE, RR>;
+  LRAMM_SP(1, 3) LRAMM_SP(2, 3) LRAMM_SP(3, 3) LRAMM_SP(4, 3) LRAMM_SP(5, 3) LRAMM_SP(6, 3) LRAMM_SP(7, 3)
+  LRAMM_SP(8, 3) LRAMM_SP(9, 3) LRAMM_SP(10, 3) LRAMM_SP(11, 3) LRAMM_SP(12, 3)
+  LRAMM_SP(1, 6) LRAMM_SP(2, 6) LRAMM_SP(3, 6) LRAMM_SP(4, 6) LRAMM_SP(5, 6) LRAMM_SP(6, 6) LRAMM_SP(7, 6)
+  LRAMM_SP(8, 6) LRAMM_SP(9, 6) LRAMM_SP(10, 6) LRAMM_SP(11, 6) LRAMM_SP(12, 6)
+  LRAMM_SP(13, 0) LRAMM_SP(14, 0) LRAMM_SP(15, 0) LRAMM_SP(16, 0) LRAMM_SP(17, 0) LRAMM_SP(18, 0)
+#undef LRAMM_SP
+  return nullptr;
 }
 
 static EigPlan plan_sytrd(int n, int batch) {
@@ -1011,34 +1140,47 @@ static EigPlan plan_sytrd(int n, int batch) {
     const char *s = getenv("LRAMM_EIG_CLUSTER");
     return s ? atoi(s) : 0;
   }();
-  if (env_reg && n <= 32 * kSytrdRegMaxE) {
-    const int E = (n + 31) / 32, rm = sytrd_rmax(E), nrw = 7;
+  if (env_reg) {
+    // push kernel: 8 warps; rows in registers (RM 3 or 6 per row warp) up to E = 12, else in
+    // shared memory; the cluster is the smallest power of two that fits
+    const int E = (n + 31) / 32, nrw = 6;
     p.ldr = (int)round_up(n, 2) + 1;
-    int pick = 0;
     auto rows_per_warp = [&](int C) { return (int)ceil_div(ceil_div(n, C), nrw); };
-    if (env_c0 > 0 && rows_per_warp(env_c0) <= rm) pick = env_c0;
-    if (!pick && batch >= 16)
-      for (int C : {1, 2, 4, 8, 16})
-        if (rows_per_warp(C) <= rm) {
+    int optin2 = 0, dev2 = 0;
+    cudaGetDevice(&dev2);
+    cudaDeviceGetAttribute(&optin2, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev2);
+    int pick = 0, rm = -1;
+    const int cands[5] = {1, 2, 4, 8, 16};
+    if (E <= kSytrdRegMaxE) {
+      for (int want : {3, 6}) {
+        for (int C : cands) {
+          if (env_c0 > 0 && C != env_c0) continue;
+          if (batch < 16 && want == 3 && C < 16 && rows_per_warp(C) > 3) continue;
+          if (rows_per_warp(C) <= want) {
+            pick = C;
+            rm = want;
+            break;
+          }
+        }
+        if (pick) break;
+      }
+    }
+    if (!pick && E <= 18) {
+      for (int C : cands) {
+        if (env_c0 > 0 && C != env_c0) continue;
+        const size_t sm = (size_t)(4 * n + 3 * p.ldr + 32 + ceil_div(n, C) * (p.ldr + 2)) * sizeof(double);
+        if (sm + 2048 <= (size_t)optin2 && (C == 16 || ceil_div(n, C) <= 40)) {
           pick = C;
+          rm = 0;
           break;
         }
-    if (!pick)
-      for (int C : {1, 2, 4, 8, 16})
-        if (rows_per_warp(C) <= std::min(rm, 3)) {
-          pick = C;
-          break;
-        }
-    if (!pick)
-      for (int C : {1, 2, 4, 8, 16})
-        if (rows_per_warp(C) <= rm) {
-          pick = C;
-          break;
-        }
+      }
+    }
     if (pick) {
       p.C = pick;
+      p.rm = rm;
       p.threads = 256;
-      p.smem = (size_t)(4 * ceil_div(n, pick) + 4 * p.ldr) * sizeof(double);
+      p.smem = (size_t)(4 * n + 3 * p.ldr + 32 + ceil_div(n, pick) * (2 + (rm == 0 ? p.ldr : 0))) * sizeof(double);
       p.ok = p.reg = true;
       return p;
     }
@@ -1161,7 +1303,7 @@ int eig_precondition_device(double *R, int n, int *jac_gate, void *ws, size_t ws
   LRAMM_TRY(dgemm_device_ex(1, n, n, n, w.Rt, n, w.Rt, n, w.G, n, w.gemm, w.gemm_bytes, st, sym));
   // tridiagonalisation
   {
-    void (*kern)(SytrdArgs) = p.reg ? sytrd_reg_pick(n) : sytrd_pick(n);
+    void (*kern)(SytrdArgs) = p.reg ? sytrd_push_pick(n, p.rm) : sytrd_pick(n);
     if (!kern) return fail(LRAMM_ERR_UNSUPPORTED, "eig preconditioner: n = %d too wide", n);
     static PerDeviceOnce once;
     LRAMM_CUDA_TRY(once.run([] {
@@ -1171,11 +1313,13 @@ int eig_precondition_device(double *R, int n, int *jac_gate, void *ws, size_t ws
         e = allow_max_dyn_smem(k);
         if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       }
-      for (int E = 1; E <= kSytrdRegMaxE && e == cudaSuccess; ++E) {
-        void (*k)(SytrdArgs) = sytrd_reg_pick(32 * E);
-        e = allow_max_dyn_smem(k);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      }
+      for (int E = 1; E <= 18 && e == cudaSuccess; ++E)
+        for (int rm : {0, 3, 6}) {
+          void (*k)(SytrdArgs) = sytrd_push_pick(32 * E, rm);
+          if (!k) continue;
+          e = allow_max_dyn_smem(k);
+          if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        }
       if (e == cudaSuccess) e = allow_max_dyn_smem(backtransform_kernel);
       if (e == cudaSuccess) e = allow_max_dyn_smem(reflector_t_kernel);
       if (e == cudaSuccess) e = allow_max_dyn_smem(tridiag_twisted_kernel);

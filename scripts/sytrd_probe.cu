@@ -10,7 +10,8 @@
 int main(int argc, char **argv) {
   int n = argc > 1 ? atoi(argv[1]) : 272;
   int C = argc > 2 ? atoi(argv[2]) : 16;
-  int warps = argc > 3 ? atoi(argv[3]) : 24;
+  int rm = argc > 3 ? atoi(argv[3]) : 3;  // rows per row warp in registers (0: shared memory)
+  int warps = 8;
   std::vector<double> h((size_t)n * n);
   std::mt19937_64 g(1);
   std::normal_distribution<double> nd;
@@ -22,8 +23,9 @@ int main(int argc, char **argv) {
   cudaMemcpy(G, h.data(), 8ull * n * n, cudaMemcpyHostToDevice);
   lramm::SytrdArgs a{G, n, (int64_t)n * n, n, d, e, tau, V, (int)(((n + 1) / 2) * 2 + 1)};
   const int nlmax = (n + C - 1) / C;
-  size_t smem = (size_t)((size_t)nlmax * a.ldr + 4 * nlmax + 4 * a.ldr) * 8;
-  void (*kern)(lramm::SytrdArgs) = lramm::sytrd_pick(n);
+  size_t smem = (size_t)(4 * n + 3 * a.ldr + 32 + (size_t)nlmax * (2 + (rm == 0 ? a.ldr : 0))) * 8;
+  void (*kern)(lramm::SytrdArgs) = lramm::sytrd_push_pick(n, rm);
+  if (!kern) { printf("no kernel for n=%d rm=%d\n", n, rm); return 1; }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
@@ -41,8 +43,9 @@ int main(int argc, char **argv) {
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     long long t[16]; cudaMemcpyFromSymbol(t, sytrd_trace, sizeof(t));
     double st = n - 3;
-    printf("n=%d C=%d warps=%d err=%s  %.1f us (%.2f us/step)  cycles/step: gather %.0f  s %.0f  hh/rows %.0f  sync %.0f  dots %.0f  cl.sync %.0f  total %.0f\n",
-           n, C, warps, cudaGetErrorString(err), ms * 1e3, ms * 1e3 / st, t[0] / st, t[1] / st, t[2] / st, t[3] / st, t[4] / st, t[5] / st, t[6] / st);
+    printf("n=%d C=%d rm=%d err=%s  %.1f us (%.2f us/step)  cycles/step: wait %.0f  s %.0f  hh/rows %.0f  sync %.0f  dots+push %.0f  -  %.0f  total %.0f\n",
+           n, C, rm, cudaGetErrorString(err), ms * 1e3, ms * 1e3 / st, t[0] / st, t[1] / st, t[2] / st, t[3] / st, t[4] / st, t[5] / st, t[6] / st);
+    printf("   hh: rr %.0f  sig2 %.0f  shfl %.0f  householder %.0f\n", t[8] / st, t[9] / st, t[10] / st, t[11] / st);
   }
   return 0;
 }
