@@ -665,6 +665,17 @@ def dominant_roofline(name, us, cfg, peaks):
                 "peak_source": FP64_PEAK_SOURCE,
                 "note": "latency-bound sequential rotation chain (w steps per sweep); traffic: columns stay in "
                         "shared memory, DRAM bytes are the one-time load of R^T"}
+    if "sytrd" in name:
+        # Householder tridiagonalisation of the w x w Gram R R^T (the eigenvector preconditioner of the
+        # small SVD): 4/3 w^3 flops in w - 2 dependent steps
+        flops = 4.0 / 3.0 * w ** 3
+        achieved = flops / (us * 1e-6) / 1e12
+        return {"bound": "tensor", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak, "traffic": None, "algorithmic_flops": flops,
+                "peak_source": FP64_PEAK_SOURCE,
+                "note": "latency-bound: w - 2 dependent reflector steps, each one DSMEM exchange (st.async + "
+                        "mbarrier) across the cluster; the matrix stays in registers / shared memory (no DRAM "
+                        "traffic beyond the one load of the Gram matrix)"}
     if "chol" in name or "trinv" in name:
         flops = w ** 3 / 3.0
         achieved = flops / (us * 1e-6) / 1e12
@@ -688,7 +699,9 @@ STAGES = (  # kernel-name fragments -> stage of the hot path (SURVEY §8(a) rows
     ("omega", ("omega",)),
     ("quantize", ("absmax", "quantize", "scales_from", "split_limbs")),
     ("int8_gemm", ("igemm", "epilogue")),
-    ("jacobi_svd", ("jacobi", "col_norms", "rank_kernel", "finalize_write", "complete_kernel", "scale_cols")),
+    ("small_svd", ("jacobi", "col_norms", "rank_kernel", "finalize_write", "complete_kernel", "scale_cols", "sytrd",
+                   "bisect", "twisted", "reflector_t", "backtransform", "eig_defect", "refine_", "offrel",
+                   "copy_if_converged")),
     ("fp64_qr", ("dgemm", "chol", "trsm", "cf_prep", "splitk", "transpose", "householder", "diag_inv",
                  "set_identity", "any_nonzero")),
 )
@@ -717,7 +730,9 @@ def stage_rooflines(per, reps, cfg, peaks, sweeps=10):
     passes = 1 if cfg.get("mode") == "fast" else 2
     qr_flops = (sum(3.0 * passes * rr * w * w for rr in sk_rows) + sum(6.0 * rr * w * w for rr in pj_rows)
                 + 2.0 * (m + k) * w * w + 2.0 * (k + n) * w * w)
-    jac_flops = 2 * sweeps * (w * (w - 1) / 2) * 8 * w
+    # small SVD (per operand): tridiagonalisation 4/3 w^3, back-transform 2 w^3, the Gram / Lowdin /
+    # rotation / check GEMMs 5 x 2 w^3 (the refinement GEMMs only run when the check fails)
+    svd_flops = 2 * (4.0 / 3.0 + 2.0 + 10.0) * w ** 3
     work = {
         "omega": (0.0, 8.0 * (k + n) * w, "bytes: Omega_A, Omega_B written (fp64)"),
         "quantize": (0.0, float(q_bytes), "bytes: fp32 operands read once + 2 int8 copies; fp64 sketch and "
@@ -726,7 +741,8 @@ def stage_rooflines(per, reps, cfg, peaks, sweeps=10):
                                                    "int8 operands read + outputs written"),
         "fp64_qr": (qr_flops / fp64, 0.0, "3 rows w^2 per CholeskyQR pass (one pass for fast-mode sketches, two "
                                           "for the projections) + the two lifts (fp64 tensor peak)"),
-        "jacobi_svd": (jac_flops / fp64, 0.0, f"{sweeps} sweeps x w(w-1)/2 pairs x 8w flops, two operands"),
+        "small_svd": (svd_flops / fp64, 0.0, "eigenvector-preconditioned SVD of the w x w R^T, two operands: "
+                                            "tridiagonalisation 4/3 w^3 + back-transform 2 w^3 + 5 GEMMs 2 w^3"),
     }
     out = {}
     for stage, frags in STAGES:

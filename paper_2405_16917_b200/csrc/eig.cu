@@ -92,21 +92,30 @@ __device__ __forceinline__ double cta_max(double v, double *red) {
 // ------------------------------------------------------------------ tridiagonalisation
 // LAPACK dsytd2 (lower) semantics: reflector k = I - tau_k v_k v_k^T acts on indices k+1..n-1,
 // v_k[k+1] = 1; d_k = T_kk, e_k = T_{k+1,k} = beta_k.  Rows of the n x n matrix are spread
-// cyclically over the C CTAs of a cluster (row i on CTA i mod C, in shared memory).  Step k:
-//   every CTA knows v_k, tau_k (computed redundantly) and holds its rows of A_k;
-//   p_i = tau_k A_k[i, k+1:] . v_k for its rows i > k is published in its own shared memory
-//   together with (owner of row k+1) the trailing part of row k+1;
-//   one cluster barrier; every CTA gathers the whole of p and row k+1 through DSMEM, forms
-//   w = p - (tau_k/2)(p.v_k) v_k, updates row k+1 to A_{k+1} (redundantly) and derives
-//   reflector k+1 from it, then updates its own rows (A -= v w^T + w v^T) fused with the next
-//   dot products.  One cluster-wide exchange per step.
+// cyclically over the C CTAs of a cluster (row i on CTA i mod C).  Step k:
+//   every CTA knows v_k, tau_k (derived redundantly) and holds its rows of A_k;
+//   it has received from every CTA (p_j, A_k[j, k+1]) for j > k, p = tau_k A_k v_k: each CTA
+//   pushes those pairs for its own rows into every CTA's receive buffer with st.async, whose
+//   bytes complete a transaction count on the receiver's mbarrier (one per buffer parity), so a
+//   CTA starts step k as soon as all rows of that step have landed -- no cluster barrier and no
+//   gather per step;
+//   s = p . v_k and w = p - (tau_k / 2) s v_k (every warp, redundantly); warp 0 updates column
+//   k+1 (= row k+1) to A_{k+1} and derives reflector k+1 from it while the other warps apply
+//   A -= v w^T + w v^T to their rows; after one CTA barrier the next p_i and A[i, k+2] of the own
+//   rows are formed and pushed.
+// Row storage per CTA: RM rows per row warp in registers (lane owns columns lane + 32 e), then
+// nsm rows in shared memory, then the rest in L2-resident global scratch (w = 1056); the
+// shared-memory / global rows are updated in one fused pass once the reflector is known.
 struct SytrdArgs {
   const double *G;  // n x n row-major (ldg), symmetric; problem stride g_stride
   int64_t ldg, g_stride;
   int n;
   double *d, *e, *tau;  // per problem: n, n, n (stride n)
   double *V;            // per problem n x n row-major: row k = v_k at columns k+1..n-1
-  int ldr;              // shared-memory row stride (doubles)
+  int ldr;              // row stride (doubles) of the shared-memory / global row storage
+  int nsm;              // rows per CTA held in shared memory (after the register rows)
+  double *Ag;           // rows beyond those: global scratch, [batch * C][ag_rows][ldr]
+  int64_t ag_rows;      // rows per CTA in Ag
 };
 
 __device__ __forceinline__ double warp_allsum(double v) {
@@ -129,261 +138,9 @@ __device__ __forceinline__ void householder(double alpha, double s2, double &bet
   }
 }
 
-__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, int rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ double ld_cluster_f64(uint32_t addr) {
-  double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
-  return v;
-}
-
-// E = elements per lane of a trailing row (n <= 32 E); every per-row loop is unrolled so its
-// shared-memory loads issue back to back.
-template <int E>
-__global__ void __launch_bounds__(640, 1) sytrd_cluster_kernel(SytrdArgs a) {
-  cg::cluster_group cl = cg::this_cluster();
-  const int C = (int)cl.num_blocks();  // a power of two
-  const int lgC = __ffs(C) - 1;
-  const int me = (int)cl.block_rank();
-  const int prob = blockIdx.x >> lgC;
-  const int n = a.n, ldr = a.ldr;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5, nth = blockDim.x;
-  const int nl = (n - me + C - 1) >> lgC;  // local rows: global i = me + li * C
-  const int nlmax = (n + C - 1) >> lgC;
-  extern __shared__ __align__(16) double sm[];
-  double2 *pub = reinterpret_cast<double2 *>(sm);              // [2][nlmax] (p_i, a_{i,k+1})
-  double *A = sm + 4 * nlmax;                                  // [nlmax][ldr]
-  double *pf = A + (size_t)nlmax * ldr;                        // [ldr] gathered p
-  double *rk = pf + ldr;                                       // [ldr] gathered column k+1 (= row k+1)
-  double *vb = rk + ldr;                                       // [2][ldr] reflectors (current / next)
-  __shared__ double red[2][32];
-  __shared__ double hh[4];  // tau_{k+1}
-
-  const double *G = a.G + (size_t)prob * a.g_stride;
-  double *dout = a.d + (size_t)prob * n, *eout = a.e + (size_t)prob * n, *tout = a.tau + (size_t)prob * n;
-  double *Vout = a.V + (size_t)prob * n * n;
-
-  // exact power-of-two prescale: largest diagonal into [1, 4)
-  double dm = 0.0;
-  for (int i = tid; i < n; i += nth) dm = fmax(dm, fabs(G[(int64_t)i * a.ldg + i]));
-  dm = cta_max(dm, red[0]);
-  double scale = 1.0;
-  if (dm > 0.0 && dm <= DBL_MAX) scale = ldexp(1.0, -2 * (ilogb(dm) >> 1));
-  for (int li = warp; li < nl; li += nwarp) {
-    const int i = me + (li << lgC);
-    const double *src = G + (int64_t)i * a.ldg;
-    for (int j = lane; j < n; j += 32) A[(size_t)li * ldr + j] = src[j] * scale;
-  }
-  for (int j = tid; j < n; j += nth) rk[j] = G[j] * scale;
-  __syncthreads();
-  double *v = vb, *vn = vb + ldr;
-  double tau;
-  {  // row 0 (redundant in every CTA) -> d_0, reflector 0
-    double s2 = 0.0;
-    for (int j = 2 + tid; j < n; j += nth) s2 = fma(rk[j], rk[j], s2);
-    s2 = cta_sum<32>(s2, red[1]);
-    double beta, scl;
-    householder(rk[1], s2, beta, tau, scl);
-    for (int j = 1 + tid; j < n; j += nth) {
-      const double vj = j == 1 ? 1.0 : rk[j] * scl;
-      v[j] = vj;
-      if (me == 0) Vout[j] = vj;
-    }
-    if (me == 0 && tid == 0) {
-      dout[0] = rk[0];
-      eout[0] = beta;
-      tout[0] = tau;
-    }
-  }
-  __syncthreads();
-  {  // p_0 and column-1 entries of own rows i >= 1
-    for (int li = warp; li < nl; li += nwarp) {
-      const int i = me + (li << lgC);
-      if (i < 1) continue;
-      const double *ar = A + (size_t)li * ldr;
-      double dot = 0.0;
-      for (int j = 1 + lane; j < n; j += 32) dot = fma(ar[j], v[j], dot);
-      dot = warp_allsum(dot);
-      if (lane == 0) pub[li] = make_double2(tau * dot, ar[1]);
-    }
-  }
-  const uint32_t pub_s = sm100::smem_u32(pub);
-  cl.sync();
-
-  for (int k = 0; k <= n - 3; ++k) {
-    const int par = k & 1, npar = par ^ 1;
-    const bool last = (k == n - 3);
-    STR_MARK(t0);
-    // ---- gather (p_j, A_k[j, k+1]) for j = k+1..n-1 through DSMEM (row j lives on CTA j mod C)
-    for (int j = k + 1 + tid; j < n; j += nth) {
-      const uint32_t pa = mapa_u32(pub_s + (par * nlmax + (j >> lgC)) * 16, j & (C - 1));
-      double pj, cj;
-      asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(pj), "=d"(cj) : "r"(pa) : "memory");
-      pf[j] = pj;
-      rk[j] = cj;
-    }
-    __syncthreads();
-    STR_MARK(t1);
-    // ---- s = p . v (every warp, redundantly); w_j = p_j - c v_j
-    const int j0 = k + 1 + lane;  // this lane's columns: j0 + 32 e
-    double pr[E], vr[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int j = j0 + 32 * e;
-      const bool in = j < n;
-      pr[e] = in ? pf[j] : 0.0;
-      vr[e] = in ? v[j] : 0.0;
-    }
-    double sacc = 0.0;
-#pragma unroll
-    for (int e = 0; e < E; ++e) sacc = fma(pr[e], vr[e], sacc);
-    const double c = 0.5 * tau * warp_allsum(sacc);
-    const double wk1 = __shfl_sync(0xffffffffu, pr[0], 0) - c;  // p_{k+1} - c v_{k+1}, v_{k+1} == 1
-    STR_MARK(t2);
-    if (warp == 0) {
-      // ---- row k+1 of A_{k+1}, d_{k+1}, reflector k+1 (warp 0; other warps update rows)
-      double r[E];
-      double s2 = 0.0;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int j = j0 + 32 * e;
-        const double rkj = j < n ? rk[j] : 0.0;
-        r[e] = rkj - fma(-c, vr[e], pr[e]) - wk1 * vr[e];
-        if (j >= k + 3 && j < n) s2 = fma(r[e], r[e], s2);
-      }
-      s2 = warp_allsum(s2);
-      const double alpha = __shfl_sync(0xffffffffu, r[0], 1);  // j = k+2
-      const double dk1 = __shfl_sync(0xffffffffu, r[0], 0);    // j = k+1
-      if (!last) {
-        double beta, tn, scl;
-        householder(alpha, s2, beta, tn, scl);
-        double *vrow = Vout + (size_t)(k + 1) * n;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int j = j0 + 32 * e;
-          if (j >= k + 2 && j < n) {
-            const double vj = j == k + 2 ? 1.0 : r[e] * scl;
-            vn[j] = vj;
-            if (me == 0) vrow[j] = vj;
-          }
-        }
-        if (lane == 0) {
-          hh[0] = tn;
-          if (me == 0) {
-            dout[k + 1] = dk1;
-            eout[k + 1] = beta;
-            tout[k + 1] = tn;
-          }
-        }
-      } else if (me == 0 && lane == 0) {
-        dout[n - 2] = dk1;
-        eout[n - 2] = alpha;
-      }
-    } else {
-      // ---- own rows i >= k+2: A -= v w^T + w v^T (columns >= k+1 of the lane layout; the
-      //      column k+1 entry is never read again)
-      int li0 = (k + 2 - me + C - 1) >> lgC;
-      if (li0 < 0) li0 = 0;
-      for (int li = li0 + warp - 1; li < nl; li += nwarp - 1) {
-        const int i = me + (li << lgC);
-        double *ar = A + (size_t)li * ldr;
-        const double vi = v[i], wi = pf[i] - c * vi;
-        double x[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int j = j0 + 32 * e;
-          x[e] = j < n ? ar[j] : 0.0;
-        }
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int j = j0 + 32 * e;
-          const double wj = fma(-c, vr[e], pr[e]);
-          const double xv = fma(-wi, vr[e], fma(-vi, wj, x[e]));
-          if (j < n) ar[j] = xv;
-        }
-        if (last && i == n - 1 && lane == 1) dout[n - 1] = ar[n - 1];  // j0 + 0 == n - 1 on lane 1
-      }
-    }
-    if (last) break;
-    STR_MARK(t3);
-    __syncthreads();
-    STR_MARK(t4);
-    // ---- p_{k+1} and the column-(k+2) entry of own rows i >= k+2
-    {
-      const double tn = hh[0];
-      double vv[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int j = j0 + 32 * e;
-        vv[e] = (j >= k + 2 && j < n) ? vn[j] : 0.0;
-      }
-      int li0 = (k + 2 - me + C - 1) >> lgC;
-      if (li0 < 0) li0 = 0;
-      for (int li = li0 + warp; li < nl; li += nwarp) {
-        const double *ar = A + (size_t)li * ldr;
-        double dot = 0.0;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int j = j0 + 32 * e;
-          dot = fma(j < n ? ar[j] : 0.0, vv[e], dot);
-        }
-        dot = warp_allsum(dot);
-        if (lane == 0) pub[npar * nlmax + li] = make_double2(tn * dot, ar[k + 2]);
-      }
-      tau = tn;
-    }
-    {
-      double *t = v;
-      v = vn;
-      vn = t;
-    }
-    STR_MARK(t5);
-    cl.sync();
-    STR_MARK(t6);
-    STR_ADD(0, t0, t1);
-    STR_ADD(1, t1, t2);
-    STR_ADD(2, t2, t3);
-    STR_ADD(3, t3, t4);
-    STR_ADD(4, t4, t5);
-    STR_ADD(5, t5, t6);
-    STR_ADD(6, t0, t6);
-  }
-  cl.sync();  // peers may still be reading this CTA's shared memory
-}
-
-// Push variant: no cluster barrier and no gather per step.  Each CTA pushes (p_i, A[i, k+2]) of
-// its rows into every CTA's receive buffer with st.async, whose bytes complete a transaction
-// count on the receiver's mbarrier (one per buffer parity); a CTA starts step k as soon as all
-// rows of that step have landed.  RM > 0: each row warp keeps up to RM rows in registers (lane
-// owns columns lane + 32 e); RM == 0: rows stay in shared memory and the update is fused with
-// the next dot products after the reflector is known.
-__device__ __forceinline__ void mbar_wait_acq_cluster(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "W_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra W_%=;\n}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void st_async_v2(uint32_t raddr, double a, double b, uint32_t rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
-               "d"(a), "d"(b), "r"(rbar)
-               : "memory");
-}
-
-__device__ __forceinline__ void st_async_f64(uint32_t raddr, double a, uint32_t rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(a),
-               "r"(rbar)
-               : "memory");
-}
-
 // dlarfg without division or square root on the chain: rs = 1/sqrt(alpha^2 + s2) (MUFU seed +
 // third-order correction), beta = -sign(alpha)/rs, tau = 1 + |alpha| rs, 1/(alpha - beta) =
-// sign(alpha) / (|alpha| + 1/rs); tiny operands take the exact library path
+// sign(alpha) / (|alpha| + 1/rs); out-of-range operands take the exact library path
 __device__ __forceinline__ void householder_fast(double alpha, double s2, double &beta, double &tau, double &scl) {
   const double t = fma(alpha, alpha, s2);
   if (s2 == 0.0) {
@@ -407,10 +164,32 @@ __device__ __forceinline__ void householder_fast(double alpha, double s2, double
   scl = copysign(rcp_nr(aa + nrm), alpha);
 }
 
-constexpr int kSytrdRegMaxE = 12;
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, double a, double b, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "d"(a), "d"(b), "r"(rbar)
+               : "memory");
+}
+
+constexpr int kSytrdRegMaxE = 12;   // register rows up to n = 384
+constexpr int kSytrdMaxE = 33;      // n <= 1056
+constexpr int kSytrdWarps = 8;
 
 template <int E, int RM>
-__global__ void __launch_bounds__(256, 1) sytrd_push_kernel(SytrdArgs a) {
+__global__ void __launch_bounds__(32 * kSytrdWarps, 1) sytrd_push_kernel(SytrdArgs a) {
   constexpr int RR = RM > 0 ? RM : 1;
   cg::cluster_group cl = cg::this_cluster();
   const int C = (int)cl.num_blocks();  // a power of two
@@ -424,18 +203,23 @@ __global__ void __launch_bounds__(256, 1) sytrd_push_kernel(SytrdArgs a) {
   const int nrw = nwarp - 2;
   const int rwi = warp == 0 || warp == 4 ? -1 : (warp < 4 ? warp - 1 : warp - 2);
   const int nl = (n - me + C - 1) >> lgC;  // local rows: global i = me + li * C
+  const int nlmax = (n + C - 1) >> lgC;
+  const int nreg = RM > 0 ? nrw * RM : 0;   // local rows li < nreg: registers (li = rwi + r * nrw)
+  const int nsm = a.nsm;                     // then shared memory, then global
   extern __shared__ __align__(16) double sm[];
   double2 *rbuf = reinterpret_cast<double2 *>(sm);  // [2][n] received (p_j, A[j, k+1])
-  double *sbuf = sm + 4 * (size_t)n;                // [2][16] received partials of s = p . v
-  double2 *stage = reinterpret_cast<double2 *>(sbuf + 32);  // [nlmax] pushes staged behind a barrier
-  double2 *pf0 = stage;
-  double *vb = sbuf + 32 + 2 * ((n + C - 1) >> lgC);  // [2][ldr]
+  double2 *stage = rbuf + 2 * (size_t)n;            // [nlmax] prologue pushes behind a barrier
+  double *vb = reinterpret_cast<double *>(stage + nlmax);  // [2][ldr]
   double *rk = vb + 2 * (size_t)ldr;                // [ldr] row 0 at start
-  double *A = rk + ldr;                             // RM == 0: [nl][ldr]
+  double *As = rk + ldr;                            // [nsm][ldr]
+  double *Ag = a.Ag ? a.Ag + (size_t)blockIdx.x * a.ag_rows * ldr : nullptr;
   __shared__ double red[2][32];
-  __shared__ double wpart[8];
   __shared__ double hh[4];
   __shared__ __align__(8) uint64_t bars[2];
+  auto row_ptr = [&](int li) {  // storage of a non-register local row
+    const int t = li - nreg;
+    return t < nsm ? As + (size_t)t * ldr : Ag + (size_t)(t - nsm) * ldr;
+  };
 
   const double *G = a.G + (size_t)prob * a.g_stride;
   double *dout = a.d + (size_t)prob * n, *eout = a.e + (size_t)prob * n, *tout = a.tau + (size_t)prob * n;
@@ -446,6 +230,7 @@ __global__ void __launch_bounds__(256, 1) sytrd_push_kernel(SytrdArgs a) {
     sm100::mbar_init(&bars[1], 1);
     sm100::fence_barrier_init();
   }
+  // exact power-of-two prescale: largest diagonal into [1, 4)
   double dm = 0.0;
   for (int i = tid; i < n; i += nth) dm = fmax(dm, fabs(G[(int64_t)i * a.ldg + i]));
   dm = cta_max(dm, red[0]);
@@ -453,26 +238,23 @@ __global__ void __launch_bounds__(256, 1) sytrd_push_kernel(SytrdArgs a) {
   if (dm > 0.0 && dm <= DBL_MAX) scale = ldexp(1.0, -2 * (ilogb(dm) >> 1));
   double x[RR][E];
   int gi[RR];
-  if (RM > 0) {
 #pragma unroll
-    for (int r = 0; r < RR; ++r) {
-      const int li = rwi + r * nrw;
-      gi[r] = (rwi >= 0 && li < nl) ? me + (li << lgC) : -1;
-      const double *src = G + (int64_t)(gi[r] < 0 ? 0 : gi[r]) * a.ldg;
+  for (int r = 0; r < RR; ++r) {
+    const int li = rwi + r * nrw;
+    gi[r] = (RM > 0 && rwi >= 0 && li < nl) ? me + (li << lgC) : -1;
+    const double *src = G + (int64_t)(gi[r] < 0 ? 0 : gi[r]) * a.ldg;
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int j = lane + 32 * e;
-        x[r][e] = (gi[r] >= 0 && j < n) ? src[j] * scale : 0.0;
-      }
-    }
-  } else {
-    for (int li = warp; li < nl; li += nwarp) {
-      const double *src = G + (int64_t)(me + (li << lgC)) * a.ldg;
-      for (int j = lane; j < n; j += 32) A[(size_t)li * ldr + j] = src[j] * scale;
+    for (int e = 0; e < E; ++e) {
+      const int j = lane + 32 * e;
+      x[r][e] = (gi[r] >= 0 && j < n) ? src[j] * scale : 0.0;
     }
   }
+  for (int li = nreg + warp; li < nl; li += nwarp) {
+    const double *src = G + (int64_t)(me + (li << lgC)) * a.ldg;
+    double *dst = row_ptr(li);
+    for (int j = lane; j < n; j += 32) dst[j] = src[j] * scale;
+  }
   for (int j = tid; j < n; j += nth) rk[j] = G[j] * scale;
-  for (int j = tid; j < 32; j += nth) sbuf[j] = 0.0;
   __syncthreads();
   double *v = vb, *vn = vb + ldr;
   double tau;
@@ -504,27 +286,19 @@ __global__ void __launch_bounds__(256, 1) sytrd_push_kernel(SytrdArgs a) {
       st_async_v2(ra, pv, cv, rb);
     }
   };
-
-  {  // p_0 and the column-1 entries of own rows i >= 1
-    double vv[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int j = lane + 32 * e;
-      vv[e] = j < n ? v[j] : 0.0;
-    }
-    // prologue runs once: dots staged, barrier, then pushes
+  {  // p_0 and the column-1 entries of own rows i >= 1 (once: dots staged, a barrier, then pushes)
     for (int li = warp; li < nl; li += nwarp) {
       const int i = me + (li << lgC);
       if (i < 1) continue;
       double dot = 0.0;
       for (int j = lane; j < n; j += 32) dot = fma(G[(int64_t)i * a.ldg + j] * scale, v[j], dot);
       dot = warp_allsum(dot);
-      if (lane == 0) pf0[li] = make_double2(tau * dot, G[(int64_t)i * a.ldg + 1] * scale);
+      if (lane == 0) stage[li] = make_double2(tau * dot, G[(int64_t)i * a.ldg + 1] * scale);
     }
     __syncthreads();
     for (int li = warp; li < nl; li += nwarp) {
       const int i = me + (li << lgC);
-      if (i >= 1) push(i, pf0[li].x, pf0[li].y, 0);
+      if (i >= 1) push(i, stage[li].x, stage[li].y, 0);
     }
   }
 
@@ -536,7 +310,7 @@ __global__ void __launch_bounds__(256, 1) sytrd_push_kernel(SytrdArgs a) {
     if (tid == 0 && !last) sm100::mbar_arrive_expect_tx(&bars[npar], 16u * (uint32_t)(n - k - 2));
     STR_MARK(t1);
     const double2 *rb = rbuf + (size_t)par * n;
-    // s = p . v from the CTAs' partials (fixed order); w_j = p_j - c v_j on this lane's columns
+    // s = p . v; w_j = p_j - c v_j on this lane's columns (zero for j <= k)
     double wr[E], vr[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -554,7 +328,6 @@ __global__ void __launch_bounds__(256, 1) sytrd_push_kernel(SytrdArgs a) {
     STR_MARK(t2);
     if (warp == 0) {
       // column k+1 of A_{k+1}: r_j = A_k[j, k+1] - v_j w_{k+1} - w_j   (v_{k+1} = 1)
-      STR_MARK(h0);
       const double wk1 = rb[k + 1].x - c;
       double rr[E];
       double s2 = 0.0;
@@ -564,9 +337,7 @@ __global__ void __launch_bounds__(256, 1) sytrd_push_kernel(SytrdArgs a) {
         rr[e] = (j > k && j < n) ? rb[j].y - wr[e] - wk1 * vr[e] : 0.0;
         if (j >= k + 3) s2 = fma(rr[e], rr[e], s2);
       }
-      STR_MARK(h1);
       s2 = warp_allsum(s2);
-      STR_MARK(h2);
       double al = 0.0, dk = 0.0;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
@@ -575,16 +346,9 @@ __global__ void __launch_bounds__(256, 1) sytrd_push_kernel(SytrdArgs a) {
       }
       const double alpha = __shfl_sync(0xffffffffu, al, (k + 2) & 31);
       const double dk1 = __shfl_sync(0xffffffffu, dk, (k + 1) & 31);
-      STR_MARK(h3);
       if (!last) {
         double beta, tn, scl;
         householder_fast(alpha, s2, beta, tn, scl);
-        STR_MARK(h4);
-        STR_ADD(12, h4, h4);
-        STR_ADD(8, h0, h1);
-        STR_ADD(9, h1, h2);
-        STR_ADD(10, h2, h3);
-        STR_ADD(11, h3, h4);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const int j = lane + 32 * e;
@@ -600,7 +364,7 @@ __global__ void __launch_bounds__(256, 1) sytrd_push_kernel(SytrdArgs a) {
         eout[n - 2] = alpha;
       }
     } else if (RM > 0) {
-      // own rows i >= k+2 in registers: A -= v w^T + w v^T
+      // own register rows i >= k+2: A -= v w^T + w v^T
 #pragma unroll
       for (int r = 0; r < RR; ++r) {
         if (gi[r] >= k + 2) {
@@ -618,10 +382,11 @@ __global__ void __launch_bounds__(256, 1) sytrd_push_kernel(SytrdArgs a) {
               if (lane + 32 * e == n - 1) dout[n - 1] = x[r][e];
           }
       }
-    } else if (last && warp == 1 && lane == 0 && ((n - 1) & (C - 1)) == me) {
-      // a_{n-1,n-1} - 2 v_{n-1} w_{n-1}
+    }
+    if (last && warp == 1 && lane == 0 && ((n - 1) & (C - 1)) == me && ((n - 1) >> lgC) >= nreg) {
+      // row n-1 outside the registers: a_{n-1,n-1} - 2 v_{n-1} w_{n-1}
       const double vl = v[n - 1], wl = rb[n - 1].x - c * vl;
-      dout[n - 1] = A[(size_t)((n - 1) >> lgC) * ldr + n - 1] - 2.0 * vl * wl;
+      dout[n - 1] = row_ptr((n - 1) >> lgC)[n - 1] - 2.0 * vl * wl;
     }
     if (last) break;
     STR_MARK(t3);
@@ -645,37 +410,36 @@ __global__ void __launch_bounds__(256, 1) sytrd_push_kernel(SytrdArgs a) {
       vv[e] = j < n ? vn[j] : 0.0;  // zero below k+2 by construction
     }
     const int ek2 = (k + 2) >> 5, lk2 = (k + 2) & 31;
-    if (RM > 0) {
-      if (rwi >= 0) {
-        double dots[RR], cols[RR];
+    if (RM > 0 && rwi >= 0) {
+      double dots[RR], cols[RR];
 #pragma unroll
-        for (int r = 0; r < RR; ++r) {
-          double dot = 0.0, ce = 0.0;
+      for (int r = 0; r < RR; ++r) {
+        double dot = 0.0, ce = 0.0;
 #pragma unroll
-          for (int e = 0; e < E; ++e) {
-            dot = fma(x[r][e], vv[e], dot);
-            if (e == ek2) ce = x[r][e];
-          }
-          dots[r] = dot;
-          cols[r] = ce;
+        for (int e = 0; e < E; ++e) {
+          dot = fma(x[r][e], vv[e], dot);
+          if (e == ek2) ce = x[r][e];
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-          for (int r = 0; r < RR; ++r) dots[r] += __shfl_xor_sync(0xffffffffu, dots[r], o);
-        }
-#pragma unroll
-        for (int r = 0; r < RR; ++r) {
-          const double ck2 = __shfl_sync(0xffffffffu, cols[r], lk2);
-          if (gi[r] >= k + 2) push(gi[r], tn * dots[r], ck2, npar);
-        }
+        dots[r] = dot;
+        cols[r] = ce;
       }
-    } else {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int r = 0; r < RR; ++r) dots[r] += __shfl_xor_sync(0xffffffffu, dots[r], o);
+      }
+#pragma unroll
+      for (int r = 0; r < RR; ++r) {
+        const double ck2 = __shfl_sync(0xffffffffu, cols[r], lk2);
+        if (gi[r] >= k + 2) push(gi[r], tn * dots[r], ck2, npar);
+      }
+    }
+    {  // shared-memory / global rows: update fused with the dot product
       int li0 = (k + 2 - me + C - 1) >> lgC;
-      if (li0 < 0) li0 = 0;
+      if (li0 < nreg) li0 = nreg;
       for (int li = li0 + warp; li < nl; li += nwarp) {
         const int i = me + (li << lgC);
-        double *ar = A + (size_t)li * ldr;
+        double *ar = row_ptr(li);
         const double vi = v[i], wi = rb[i].x - c * vi;
         double dot = 0.0, ce = 0.0;
 #pragma unroll
@@ -900,9 +664,9 @@ constexpr int kBtCols = 8;
 // T_b of every block (one CTA each): G_ac = v_a . v_c (a < c), then row a of T by the forward
 // recurrence T[a][c] = -tau_c sum_{a <= b < c} T[a][b] G_bc, T[a][a] = tau_a
 __global__ void __launch_bounds__(256) reflector_t_kernel(const double *__restrict__ Vall,
-                                                          const double *__restrict__ tauall, int n,
+                                                          const double *__restrict__ tauall, int n, int jchunk,
                                                           double *__restrict__ Tall) {
-  extern __shared__ __align__(16) double vs[];  // [kNB][n - k0]
+  extern __shared__ __align__(16) double vs[];  // [kNB][jchunk] columns of the block's vectors
   __shared__ double Gs[kNB][kNB + 1];
   __shared__ double Ts[kNB][kNB + 1];
   const int prob = blockIdx.y, blk = blockIdx.x;
@@ -910,21 +674,27 @@ __global__ void __launch_bounds__(256) reflector_t_kernel(const double *__restri
   const double *V = Vall + (size_t)prob * n * n;
   const double *tau = tauall + (size_t)prob * n;
   double *T = Tall + ((size_t)prob * nblk + blk) * kNB * kNB;
-  const int k0 = blk * kNB, nb = min(kNB, n - 2 - k0), len = n - k0;
+  const int k0 = blk * kNB, nb = min(kNB, n - 2 - k0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
-  for (int t = tid; t < kNB * len; t += blockDim.x) {
-    const int r = t / len, j = t % len;
-    vs[t] = r < nb ? V[(size_t)(k0 + r) * n + k0 + j] : 0.0;  // zeros left of each vector's start
-  }
-  __syncthreads();
-  for (int pr = warp; pr < kNB * kNB; pr += nwarp) {
-    const int aa = pr / kNB, cc = pr % kNB;
-    if (aa >= cc || cc >= nb) continue;
-    const double *va = vs + (size_t)aa * len, *vc = vs + (size_t)cc * len;
-    double sacc = 0.0;
-    for (int j = cc + 1 + lane; j < len; j += 32) sacc = fma(va[j], vc[j], sacc);
-    sacc = warp_allsum(sacc);
-    if (lane == 0) Gs[aa][cc] = sacc;
+  for (int t = tid; t < kNB * (kNB + 1); t += blockDim.x) Gs[t / (kNB + 1)][t % (kNB + 1)] = 0.0;
+  // G_ac = v_a . v_c (a < c) over column chunks of the vectors (zero left of each start)
+  for (int j0 = k0; j0 < n; j0 += jchunk) {
+    const int len = min(jchunk, n - j0);
+    __syncthreads();
+    for (int t = tid; t < kNB * len; t += blockDim.x) {
+      const int r = t / len, j = j0 + t % len;
+      vs[(size_t)r * jchunk + (j - j0)] = (r < nb && j > k0 + r) ? V[(size_t)(k0 + r) * n + j] : 0.0;
+    }
+    __syncthreads();
+    for (int pr = warp; pr < kNB * kNB; pr += nwarp) {
+      const int aa = pr / kNB, cc = pr % kNB;
+      if (aa >= cc || cc >= nb) continue;
+      const double *va = vs + (size_t)aa * jchunk, *vc = vs + (size_t)cc * jchunk;
+      double sacc = 0.0;
+      for (int j = lane; j < len; j += 32) sacc = fma(va[j], vc[j], sacc);
+      sacc = warp_allsum(sacc);
+      if (lane == 0) Gs[aa][cc] += sacc;  // the same warp owns this pair in every chunk
+    }
   }
   __syncthreads();
   if (tid < kNB) {
@@ -946,10 +716,10 @@ __global__ void __launch_bounds__(256) reflector_t_kernel(const double *__restri
 // identity when the preconditioner failed (flags[0] != 0)
 __global__ void __launch_bounds__(256) backtransform_kernel(const double *__restrict__ Zall,
                                                             const double *__restrict__ Vall,
-                                                            const double *__restrict__ Tall, int n,
+                                                            const double *__restrict__ Tall, int n, int jchunk,
                                                             const int *__restrict__ flags,
                                                             double *__restrict__ V0all) {
-  extern __shared__ __align__(16) double zs[];  // [n][kBtCols], then vsb[kNB][n] (block rows)
+  extern __shared__ __align__(16) double zs[];  // [n][kBtCols], then vsb[kNB][jchunk]
   double *vsb = zs + (size_t)n * kBtCols;
   __shared__ double w1[kNB][kBtCols];
   __shared__ double w2[kNB][kBtCols];
@@ -975,30 +745,32 @@ __global__ void __launch_bounds__(256) backtransform_kernel(const double *__rest
     zs[t] = c < n ? Z[(size_t)j * n + c] : 0.0;
   }
   const int sc = tid % kBtCols, rc = tid / kBtCols;  // 256 threads: 32 x kBtCols
+  // stage columns [j0, j0 + len) of the block's vectors (zero left of each vector's start)
+  auto stage = [&](int k0, int nb, int j0, int len) {
+    for (int t = tid; t < kNB * len; t += blockDim.x) {
+      const int r = t / len, j = j0 + t % len;
+      vsb[(size_t)r * jchunk + (j - j0)] = (r < nb && j > k0 + r) ? V[(size_t)(k0 + r) * n + j] : 0.0;
+    }
+  };
   for (int blk = nblk - 1; blk >= 0; --blk) {
     const int k0 = blk * kNB, nb = min(kNB, n - 2 - k0);
     for (int t = tid; t < kNB * kNB; t += blockDim.x) ts[t / kNB][t % kNB] = Tb[(size_t)blk * kNB * kNB + t];
-    for (int t = tid; t < nb * n; t += blockDim.x) {  // rows k0..k0+nb-1 of V (zero left of k0+r+1)
-      const int r = t / n, j = t % n;
-      vsb[t] = j > k0 + r ? V[(size_t)(k0 + r) * n + j] : 0.0;
-    }
-    __syncthreads();
-    // W1[c][s] = v_{k0+c} . Z[:, s]  (v_{k0+c} nonzero from k0+c+1)
-    {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      if (rc < nb) {
-        const double *vr = vsb + (size_t)rc * n;
-        int j = k0 + rc + 1;
-        for (; j + 3 < n; j += 4) {
-          a0 = fma(vr[j], zs[j * kBtCols + sc], a0);
-          a1 = fma(vr[j + 1], zs[(j + 1) * kBtCols + sc], a1);
-          a2 = fma(vr[j + 2], zs[(j + 2) * kBtCols + sc], a2);
-          a3 = fma(vr[j + 3], zs[(j + 3) * kBtCols + sc], a3);
-        }
-        for (; j < n; ++j) a0 = fma(vr[j], zs[j * kBtCols + sc], a0);
+    // W1[c][s] = v_{k0+c} . Z[:, s]
+    double a0 = 0.0, a1 = 0.0;
+    for (int j0 = k0 + 1; j0 < n; j0 += jchunk) {
+      const int len = min(jchunk, n - j0);
+      __syncthreads();
+      stage(k0, nb, j0, len);
+      __syncthreads();
+      const double *vr = vsb + (size_t)rc * jchunk;
+      int j = 0;
+      for (; j + 1 < len; j += 2) {
+        a0 = fma(vr[j], zs[(j0 + j) * kBtCols + sc], a0);
+        a1 = fma(vr[j + 1], zs[(j0 + j + 1) * kBtCols + sc], a1);
       }
-      w1[rc][sc] = (a0 + a1) + (a2 + a3);
+      if (j < len) a0 = fma(vr[j], zs[(j0 + j) * kBtCols + sc], a0);
     }
+    w1[rc][sc] = a0 + a1;
     __syncthreads();
     // W2 = T_b W1
     {
@@ -1006,13 +778,18 @@ __global__ void __launch_bounds__(256) backtransform_kernel(const double *__rest
       for (int c = rc; c < nb; ++c) acc = fma(ts[rc][c], w1[c][sc], acc);
       w2[rc][sc] = acc;
     }
-    __syncthreads();
-    // Z[j][s] -= sum_c v_{k0+c}[j] W2[c][s]  (j > k0 + c)
-    for (int j = k0 + 1 + rc; j < n; j += kNB) {
-      const int cmax = min(nb, j - k0);
-      double acc = 0.0;
-      for (int c = 0; c < cmax; ++c) acc = fma(vsb[(size_t)c * n + j], w2[c][sc], acc);
-      zs[j * kBtCols + sc] -= acc;
+    // Z[j][s] -= sum_c v_{k0+c}[j] W2[c][s]
+    for (int j0 = k0 + 1; j0 < n; j0 += jchunk) {
+      const int len = min(jchunk, n - j0);
+      __syncthreads();
+      stage(k0, nb, j0, len);
+      __syncthreads();
+      for (int jj = rc; jj < len; jj += kNB) {
+        const int j = j0 + jj, cmax = min(nb, j - k0);
+        double acc = 0.0;
+        for (int c = 0; c < cmax; ++c) acc = fma(vsb[(size_t)c * jchunk + jj], w2[c][sc], acc);
+        zs[j * kBtCols + sc] -= acc;
+      }
     }
     __syncthreads();
   }
@@ -1096,27 +873,13 @@ __global__ void jacobi_gate_kernel(const int *flags, int *gate, int batch) {
 
 // ================================================================== host side
 struct EigPlan {
-  int C = 0, threads = 0, ldr = 0;
+  int C = 0, threads = 0, ldr = 0, rm = 0, nsm = 0;
+  int64_t ag_rows = 0;  // rows per CTA in global scratch
   size_t smem = 0;
   bool ok = false;
-  bool reg = false;  // st.async push variant (sytrd_push_kernel)
-  int rm = 0;
 };
 
-constexpr int kSytrdMaxE = 18;  // n <= 576
-static void (*sytrd_pick(int n))(SytrdArgs) {
-  switch ((n + 31) / 32) {
-#define LRAMM_SYTRD_E(EE) \
-  case EE: return sytrd_cluster_kernel<EE>;
-    LRAMM_SYTRD_E(1) LRAMM_SYTRD_E(2) LRAMM_SYTRD_E(3) LRAMM_SYTRD_E(4) LRAMM_SYTRD_E(5) LRAMM_SYTRD_E(6)
-    LRAMM_SYTRD_E(7) LRAMM_SYTRD_E(8) LRAMM_SYTRD_E(9) LRAMM_SYTRD_E(10) LRAMM_SYTRD_E(11) LRAMM_SYTRD_E(12)
-    LRAMM_SYTRD_E(13) LRAMM_SYTRD_E(14) LRAMM_SYTRD_E(15) LRAMM_SYTRD_E(16) LRAMM_SYTRD_E(17) LRAMM_SYTRD_E(18)
-#undef LRAMM_SYTRD_E
-    default: return nullptr;
-  }
-}
-
-// sytrd_push_kernel<E, RM>: RM rows per row warp in registers (0: rows in shared memory)
+// sytrd_push_kernel<E, RM>: RM rows per row warp in registers (0: none)
 static void (*sytrd_push_pick(int n, int rm))(SytrdArgs) {
   const int E = (n + 31) / 32;
 #define LRAMM_SP(EE, RR) \
@@ -1126,105 +889,65 @@ static void (*sytrd_push_pick(int n, int rm))(SytrdArgs) {
   LRAMM_SP(1, 6) LRAMM_SP(2, 6) LRAMM_SP(3, 6) LRAMM_SP(4, 6) LRAMM_SP(5, 6) LRAMM_SP(6, 6) LRAMM_SP(7, 6)
   LRAMM_SP(8, 6) LRAMM_SP(9, 6) LRAMM_SP(10, 6) LRAMM_SP(11, 6) LRAMM_SP(12, 6)
   LRAMM_SP(13, 0) LRAMM_SP(14, 0) LRAMM_SP(15, 0) LRAMM_SP(16, 0) LRAMM_SP(17, 0) LRAMM_SP(18, 0)
+  LRAMM_SP(19, 0) LRAMM_SP(20, 0) LRAMM_SP(21, 0) LRAMM_SP(22, 0) LRAMM_SP(23, 0) LRAMM_SP(24, 0)
+  LRAMM_SP(25, 0) LRAMM_SP(26, 0) LRAMM_SP(27, 0) LRAMM_SP(28, 0) LRAMM_SP(29, 0) LRAMM_SP(30, 0)
+  LRAMM_SP(31, 0) LRAMM_SP(32, 0) LRAMM_SP(33, 0)
 #undef LRAMM_SP
   return nullptr;
 }
 
+static size_t sytrd_fixed_smem(int n, int C, int ldr) {
+  return (size_t)(4 * (int64_t)n + 2 * ceil_div(n, C) + 3 * (int64_t)ldr) * sizeof(double);
+}
+
+// Row placement: up to n = 384 every row lives in registers (3 or 6 per row warp, the cluster
+// the smallest power of two that allows it; batched problems prefer fewer CTAs each); wider
+// problems use a 16-CTA cluster with the rows in shared memory, spilling to L2-resident global
+// scratch when they do not fit (w = 1056: 66 rows per CTA, ~20 in shared memory).
 static EigPlan plan_sytrd(int n, int batch) {
   EigPlan p;
-  static const int env_reg = [] {
-    const char *s = getenv("LRAMM_EIG_REG");
-    return s ? atoi(s) : 1;
-  }();
-  static const int env_c0 = [] {
-    const char *s = getenv("LRAMM_EIG_CLUSTER");
-    return s ? atoi(s) : 0;
-  }();
-  if (env_reg) {
-    // push kernel: 8 warps; rows in registers (RM 3 or 6 per row warp) up to E = 12, else in
-    // shared memory; the cluster is the smallest power of two that fits
-    const int E = (n + 31) / 32, nrw = 6;
-    p.ldr = (int)round_up(n, 2) + 1;
-    auto rows_per_warp = [&](int C) { return (int)ceil_div(ceil_div(n, C), nrw); };
-    int optin2 = 0, dev2 = 0;
-    cudaGetDevice(&dev2);
-    cudaDeviceGetAttribute(&optin2, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev2);
-    int pick = 0, rm = -1;
-    const int cands[5] = {1, 2, 4, 8, 16};
-    if (E <= kSytrdRegMaxE) {
-      for (int want : {3, 6}) {
-        for (int C : cands) {
-          if (env_c0 > 0 && C != env_c0) continue;
-          if (batch < 16 && want == 3 && C < 16 && rows_per_warp(C) > 3) continue;
-          if (rows_per_warp(C) <= want) {
-            pick = C;
-            rm = want;
-            break;
-          }
-        }
-        if (pick) break;
-      }
-    }
-    if (!pick && E <= 18) {
-      for (int C : cands) {
-        if (env_c0 > 0 && C != env_c0) continue;
-        const size_t sm = (size_t)(4 * n + 3 * p.ldr + 32 + ceil_div(n, C) * (p.ldr + 2)) * sizeof(double);
-        if (sm + 2048 <= (size_t)optin2 && (C == 16 || ceil_div(n, C) <= 40)) {
-          pick = C;
-          rm = 0;
-          break;
-        }
-      }
-    }
-    if (pick) {
-      p.C = pick;
-      p.rm = rm;
-      p.threads = 256;
-      p.smem = (size_t)(4 * n + 3 * p.ldr + 32 + ceil_div(n, pick) * (2 + (rm == 0 ? p.ldr : 0))) * sizeof(double);
-      p.ok = p.reg = true;
-      return p;
-    }
-  }
-  int optin = 0, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t budget = (size_t)optin - 2048;
-  p.ldr = (int)round_up(n, 2) + 1;  // odd stride: column-strided lane accesses spread banks
-  auto smem_for = [&](int C) {
-    const int nlmax = (int)ceil_div(n, C);
-    return (size_t)((size_t)nlmax * p.ldr + 4 * nlmax + 4 * p.ldr) * sizeof(double);
-  };
   static const int env_c = [] {
     const char *s = getenv("LRAMM_EIG_CLUSTER");
     return s ? atoi(s) : 0;
   }();
-  int pick = 0;
-  if (env_c > 0 && smem_for(env_c) <= budget) pick = env_c;
-  if (!pick && batch >= 16 && smem_for(1) <= budget) pick = 1;  // batched: one CTA per problem
-  if (!pick)
-    for (int C : {1, 2, 4, 8, 16})
-      if (smem_for(C) <= budget && ceil_div(n, C) <= 24) {
-        pick = C;
-        break;
+  const int E = (n + 31) / 32, nrw = kSytrdWarps - 2;
+  if (E > kSytrdMaxE) return p;
+  int optin = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t budget = (size_t)optin - 4096;
+  p.ldr = (int)round_up(n, 2) + 1;
+  auto rows_per_warp = [&](int C) { return (int)ceil_div(ceil_div(n, C), nrw); };
+  const int cands[5] = {1, 2, 4, 8, 16};
+  int pick = 0, rm = 0;
+  if (E <= kSytrdRegMaxE) {
+    for (int want : {3, 6}) {
+      for (int C : cands) {
+        if (env_c > 0 && C != env_c) continue;
+        if (batch < 16 && want == 3 && C < 16 && rows_per_warp(C) > 3) continue;
+        if (rows_per_warp(C) <= want && sytrd_fixed_smem(n, C, p.ldr) <= budget) {
+          pick = C;
+          rm = want;
+          break;
+        }
       }
-  if (!pick)
-    for (int C : {16, 8})
-      if (smem_for(C) <= budget) {
-        pick = C;
-        break;
-      }
-  if (!pick || n > 32 * kSytrdMaxE) return p;
+      if (pick) break;
+    }
+  }
+  if (!pick) {
+    pick = env_c > 0 ? env_c : 16;
+    rm = 0;
+  }
+  const size_t fixed = sytrd_fixed_smem(n, pick, p.ldr);
+  if (fixed > budget) return p;
+  const int64_t rows = ceil_div(n, pick) - (int64_t)nrw * rm;
+  p.nsm = (int)std::max<int64_t>(0, std::min<int64_t>(rows, (int64_t)((budget - fixed) / (p.ldr * sizeof(double)))));
+  p.ag_rows = std::max<int64_t>(0, rows - p.nsm);
   p.C = pick;
-  p.smem = smem_for(pick);
-  const int rows = (int)ceil_div(n, pick);
-  int warps = std::min(20, std::max(8, rows + 1));  // warp 0 + one warp per row where possible
-  static const int env_w = [] {
-    const char *s = getenv("LRAMM_EIG_WARPS");
-    return s ? atoi(s) : 0;
-  }();
-  if (env_w > 0) warps = std::min(20, std::max(2, env_w));
-  p.threads = 32 * warps;
-  p.ok = true;
+  p.rm = rm;
+  p.threads = 32 * kSytrdWarps;
+  p.smem = fixed + (size_t)p.nsm * p.ldr * sizeof(double);
+  p.ok = sytrd_push_pick(n, rm) != nullptr;
   return p;
 }
 
@@ -1248,7 +971,7 @@ bool eig_precondition_enabled(int n, int batch) {
 }
 
 struct EigWs {
-  double *Rt, *G, *V, *Z, *D, *Zo, *V0, *P, *S, *E, *P2, *d, *e, *tau, *lam, *T, *gemm;
+  double *Rt, *G, *V, *Z, *D, *Zo, *V0, *P, *S, *E, *P2, *d, *e, *tau, *lam, *T, *gemm, *Ag;
   int *flags;
   size_t gemm_bytes;
 };
@@ -1274,6 +997,8 @@ static EigWs carve_eig(Arena &ar, int n, int batch) {
   w.flags = ar.take<int>(4 * batch);
   w.gemm_bytes = std::max(dgemm_ws_bytes(1, n, n, n), dgemm_ws_bytes(0, n, n, n));
   w.gemm = ar.take<double>((int64_t)(w.gemm_bytes / 8 + 1));
+  const EigPlan pl = plan_sytrd(n, batch);
+  w.Ag = pl.ag_rows > 0 ? ar.take<double>((int64_t)batch * pl.C * pl.ag_rows * pl.ldr) : nullptr;
   return w;
 }
 
@@ -1303,17 +1028,12 @@ int eig_precondition_device(double *R, int n, int *jac_gate, void *ws, size_t ws
   LRAMM_TRY(dgemm_device_ex(1, n, n, n, w.Rt, n, w.Rt, n, w.G, n, w.gemm, w.gemm_bytes, st, sym));
   // tridiagonalisation
   {
-    void (*kern)(SytrdArgs) = p.reg ? sytrd_push_pick(n, p.rm) : sytrd_pick(n);
+    void (*kern)(SytrdArgs) = sytrd_push_pick(n, p.rm);
     if (!kern) return fail(LRAMM_ERR_UNSUPPORTED, "eig preconditioner: n = %d too wide", n);
     static PerDeviceOnce once;
     LRAMM_CUDA_TRY(once.run([] {
       cudaError_t e = cudaSuccess;
-      for (int E = 1; E <= kSytrdMaxE && e == cudaSuccess; ++E) {
-        void (*k)(SytrdArgs) = sytrd_pick(32 * E);
-        e = allow_max_dyn_smem(k);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      }
-      for (int E = 1; E <= 18 && e == cudaSuccess; ++E)
+      for (int E = 1; E <= kSytrdMaxE && e == cudaSuccess; ++E)
         for (int rm : {0, 3, 6}) {
           void (*k)(SytrdArgs) = sytrd_push_pick(32 * E, rm);
           if (!k) continue;
@@ -1335,6 +1055,9 @@ int eig_precondition_device(double *R, int n, int *jac_gate, void *ws, size_t ws
     a.tau = w.tau;
     a.V = w.V;
     a.ldr = p.ldr;
+    a.nsm = p.nsm;
+    a.Ag = p.ag_rows > 0 ? w.Ag : nullptr;
+    a.ag_rows = p.ag_rows;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(p.C * batch));
     cfg.blockDim = dim3((unsigned)p.threads);
@@ -1376,10 +1099,18 @@ int eig_precondition_device(double *R, int n, int *jac_gate, void *ws, size_t ws
   }
   {
     const int nblk = (int)ceil_div(n - 2, kNB);
-    reflector_t_kernel<<<dim3((unsigned)nblk, batch), 256, (size_t)kNB * n * sizeof(double), st>>>(w.V, w.tau, n, w.T);
+    int optin = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int64_t budget = optin - 24 * 1024;  // static shared memory of the two kernels: < 17 KB
+    const int jt = (int)std::min<int64_t>(n, budget / (kNB * 8));
+    reflector_t_kernel<<<dim3((unsigned)nblk, batch), 256, (size_t)kNB * jt * sizeof(double), st>>>(w.V, w.tau, n, jt,
+                                                                                                 w.T);
     LRAMM_LAUNCH_CHECK();
-    backtransform_kernel<<<dim3((unsigned)ceil_div(n, kBtCols), batch), 256, (size_t)n * (kBtCols + kNB) * sizeof(double), st>>>(
-        w.Zo, w.V, w.T, n, w.flags, w.V0);
+    const int jb = (int)std::min<int64_t>(n, (budget - (int64_t)n * kBtCols * 8) / (kNB * 8));
+    backtransform_kernel<<<dim3((unsigned)ceil_div(n, kBtCols), batch), 256,
+                           (size_t)(n * kBtCols + kNB * jb) * sizeof(double), st>>>(w.Zo, w.V, w.T, n, jb, w.flags,
+                                                                                    w.V0);
     LRAMM_LAUNCH_CHECK();
   }
   // P = W V0 = Rt V0 (row-major P == W' as a plain matrix); check; one-sided refinement only

@@ -141,12 +141,41 @@ def integer_matmul(qa, qb):
     if qa.cols != qb.rows:
         raise ShapeError(f"inner dimensions differ: {tuple(qa.data.shape)} @ {tuple(qb.data.shape)}")
     _check_overflow(qa.cols, qa.bits, qb.bits)
+    if _is_cuda(qa.data):
+        return _imatmul_device(qa.data, qb.data, qa.bits, qb.bits)
     from . import kernels
 
-    a = qa.data.cpu().numpy() if _is_cuda(qa.data) else qa.data
-    b = qb.data.cpu().numpy() if _is_cuda(qb.data) else qb.data
-    out = kernels.imatmul(np.ascontiguousarray(a, dtype=np.int32), np.ascontiguousarray(b, dtype=np.int32))
-    return torch.from_numpy(out).to(qa.data.device) if _is_cuda(qa.data) else out
+    a, b = qa.data, qb.data
+    return kernels.imatmul(np.ascontiguousarray(a, dtype=np.int32), np.ascontiguousarray(b, dtype=np.int32))
+
+
+def _imatmul_device(a32: torch.Tensor, b32: torch.Tensor, bits_a: int, bits_b: int) -> torch.Tensor:
+    """Exact int64 A . B of device int32 quantised data (entries within +-bit_cap): 8-bit limb
+    planes through the tcgen05 kernel, accumulated exactly in int64 (the raw-product epilogue),
+    the device counterpart of _kernels.imatmul (_core.pyx:35-50) with no host round trip."""
+    dev = a32.device
+    m, k = a32.shape
+    n = b32.shape[1]
+    la, lb = limbs_for(bits_a), limbs_for(bits_b)
+    ldk = ((k + 15) // 16) * 16
+    ap = torch.zeros((m, ldk), dtype=torch.int32, device=dev)
+    ap[:, :k] = a32
+    bt = torch.zeros((n, ldk), dtype=torch.int32, device=dev)
+    bt[:, :k] = b32.T  # B^T: n x k, K-major
+    qa = torch.empty((la, m, ldk), dtype=torch.int8, device=dev)
+    qb = torch.empty((lb, n, ldk), dtype=torch.int8, device=dev)
+    st = stream_handle(dev)
+    N.check(N.LIB.lramm_split_limbs(ptr(ap), m, k, ldk, la, ptr(qa), ldk, st))
+    N.check(N.LIB.lramm_split_limbs(ptr(bt), n, k, ldk, lb, ptr(qb), ldk, st))
+    out = torch.empty((m, n), dtype=torch.int64, device=dev)
+    acc64 = torch.empty((m, n), dtype=torch.int64, device=dev)
+    e = N.Epilogue()
+    e.out_dtype = N.I64
+    e.out = out.data_ptr()
+    e.ldo = n
+    N.check(N.LIB.lramm_igemm_limbs(m, n, k, ptr(qa), qa.stride(1), qa.stride(0), la, ptr(qb), qb.stride(1),
+                                    qb.stride(0), lb, ptr(acc64), ctypes.byref(e), st))
+    return out
 
 
 def qgemm_device(a: torch.Tensor, b: torch.Tensor, bits_a: int, bits_b: int, alpha=1.0, beta=0.0, c=None,

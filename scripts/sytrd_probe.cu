@@ -23,7 +23,8 @@ int main(int argc, char **argv) {
   cudaMemcpy(G, h.data(), 8ull * n * n, cudaMemcpyHostToDevice);
   lramm::SytrdArgs a{G, n, (int64_t)n * n, n, d, e, tau, V, (int)(((n + 1) / 2) * 2 + 1)};
   const int nlmax = (n + C - 1) / C;
-  size_t smem = (size_t)(4 * n + 3 * a.ldr + 32 + (size_t)nlmax * (2 + (rm == 0 ? a.ldr : 0))) * 8;
+  const int srows = nlmax - 6 * rm > 0 ? nlmax - 6 * rm : 0;
+  size_t smem = (size_t)(4 * n + 3 * a.ldr + 2 * (size_t)nlmax + (size_t)srows * a.ldr) * 8; a.nsm = srows; a.Ag = nullptr; a.ag_rows = 0;
   void (*kern)(lramm::SytrdArgs) = lramm::sytrd_push_pick(n, rm);
   if (!kern) { printf("no kernel for n=%d rm=%d\n", n, rm); return 1; }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

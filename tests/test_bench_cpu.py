@@ -33,11 +33,11 @@ def test_stage_rooflines_classify_and_bound():
         "Memset (Device)": [10.0 * 5, 100],
     }
     st = bench.stage_rooflines(per, 5, bench.CONFIGS["c2"], {"hbm_gbs": 6500.0})
-    assert st["jacobi_svd"]["us_per_step"] == 2000.0
+    assert st["small_svd"]["us_per_step"] == 2000.0
     assert st["int8_gemm"]["us_per_step"] == 190.0
     assert st["quantize"]["us_per_step"] == 70.0
     assert st["fp64_qr"]["us_per_step"] == 800.0
     assert st["other"]["us_per_step"] == 10.0
-    for k in ("quantize", "int8_gemm", "fp64_qr", "jacobi_svd"):
+    for k in ("quantize", "int8_gemm", "fp64_qr", "small_svd"):
         assert 0.0 < st[k]["frac"] and st[k]["roofline_us"] > 0.0
-    assert st["quantize"]["bound"] == "hbm" and st["jacobi_svd"]["bound"] == "fp64"
+    assert st["quantize"]["bound"] == "hbm" and st["small_svd"]["bound"] == "fp64"

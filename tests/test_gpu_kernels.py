@@ -284,6 +284,20 @@ def test_integer_matmul_and_dequantize(L):
     assert np.array_equal(d, O.dequantize(*O.quantize_tensor(a, 8)))
 
 
+@pytest.mark.parametrize("bits,k", [(8, 300), (16, 1000), (24, 70000)])
+def test_integer_matmul_device_tensors(L, bits, k):
+    # CUDA-tensor operands stay on the device (limb planes + exact int64 epilogue), bit-exact
+    import torch
+
+    a = O.generate(9, k, "normal", 81)
+    b = O.generate(k, 7, "normal", 82)
+    qa, qb = L.quantize(torch.tensor(a, device="cuda"), bits), L.quantize(torch.tensor(b, device="cuda"), bits)
+    out = L.integer_matmul(qa, qb)
+    assert out.is_cuda and out.dtype == torch.int64
+    ref = O.imatmul(*[O.quantize_tensor(x, bits)[0] for x in (a, b)])
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
 # ------------------------------------------------------------------ fp64 building blocks
 
 
