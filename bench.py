@@ -835,6 +835,9 @@ def accuracy(L, cfg, a, b, d_ours, params, d_ref=None):
     d_rest = torch.from_numpy(O.lramm(ha, hb, O.OracleParams(**kw, spec=spec))).to(exact.device)
     out["fast_mode_rel_diff_vs_restatement"] = float(torch.linalg.norm(d_ours.double() - d_rest) /
                                                      torch.linalg.norm(d_rest))
+    if d_ours.dtype == torch.float32:  # the floor: D itself rounded to fp32
+        out["fp32_rounding_of_restatement"] = float(torch.linalg.norm(d_rest.float().double() - d_rest) /
+                                                    torch.linalg.norm(d_rest))
     out["restatement_s"] = time.perf_counter() - t0
     if d_ref is not None:
         dr = torch.from_numpy(np.ascontiguousarray(d_ref)).to(exact.device)
