@@ -481,18 +481,26 @@ __global__ void __launch_bounds__(32 * kSytrdWarps, 1) sytrd_push_kernel(SytrdAr
 // critical path per step is one FMA), rescaled by a power of two every 8 steps; the count is
 // the number of sign changes (sign bits; an exact zero is vanishingly rare at these shifts and
 // only moves the bracket by the point spacing).
-constexpr int kBisNCH = 2;
-constexpr int kBisRounds = 9;  // (32 * 2 + 1)^9 > 2^54
+constexpr int kBisRounds = 9;  // 65-section: 65^9 > 2^54
+constexpr int kBisWpe = 2;     // warps per eigenvalue (each lane follows one shift)
 
 __device__ __forceinline__ int sgnbit(double x) { return (int)((unsigned)__double2hiint(x) >> 31); }
 __device__ __forceinline__ int bexp(double x) { return (__double2hiint(x) >> 20) & 0x7ff; }
 
+// Multisection on Sturm counts: kBisWpe warps per eigenvalue index i (ascending), one shift per
+// lane; a round splits the bracket into 32 kBisWpe + 1 parts.  Counts come from the
+// leading-minor recurrence p_j = (d_j - x) p_{j-1} - e_{j-1}^2 p_{j-2} (no division; the
+// critical path per step is one FMA), rescaled by a power of two every 8 steps; the count is
+// the number of sign changes (sign bits; an exact zero is vanishingly rare at these shifts and
+// only moves the bracket by the point spacing).  Two warps per eigenvalue put two latency-bound
+// chains on each SM sub-partition.
 __global__ void __launch_bounds__(256) tridiag_bisect_kernel(const double *__restrict__ dall,
                                                              const double *__restrict__ eall, int n,
                                                              double *__restrict__ lamall) {
   extern __shared__ __align__(16) double sh[];
   double2 *sde = reinterpret_cast<double2 *>(sh);  // (d_j, e_{j-1}^2)
   __shared__ double red[32];
+  __shared__ int cnt_part[8];
   const int prob = blockIdx.y;
   const double *d = dall + (size_t)prob * n, *e = eall + (size_t)prob * n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -510,55 +518,49 @@ __global__ void __launch_bounds__(256) tridiag_bisect_kernel(const double *__res
   const double span = fmax(hi_b - lo_b, DBL_MIN);
   lo_b -= 4.0 * DBL_EPSILON * span + DBL_MIN;
   hi_b += 4.0 * DBL_EPSILON * span + DBL_MIN;
-  const int i = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (i >= n) return;
+  const int epb = (blockDim.x >> 5) / kBisWpe;  // eigenvalues per block
+  const int slot = warp / kBisWpe, h = warp % kBisWpe;
+  const int i = blockIdx.x * epb + slot;
+  const bool active = i < n;
   double lo = lo_b, hi = hi_b;
-  constexpr int NP = 32 * kBisNCH;  // interior points per round
+  constexpr int NP = 32 * kBisWpe;  // interior points per round
   for (int round = 0; round < kBisRounds; ++round) {
-    double nx[kBisNCH], p1[kBisNCH], p2[kBisNCH];
-    int cnt[kBisNCH], ng[kBisNCH];
-    const double h = (hi - lo) / (double)(NP + 1);
-    const double d0 = sde[0].x;
-#pragma unroll
-    for (int t = 0; t < kBisNCH; ++t) {
-      nx[t] = -fma((double)(1 + lane + 32 * t), h, lo);
-      p2[t] = 1.0;
-      p1[t] = d0 + nx[t];
-      ng[t] = sgnbit(p1[t]);
-      cnt[t] = ng[t];
-    }
+    const double hs = (hi - lo) / (double)(NP + 1);
+    const double nx = -fma((double)(1 + kBisWpe * lane + h), hs, lo);
+    double p2 = 1.0, p1 = sde[0].x + nx;
+    int ng = sgnbit(p1), cnt = ng;
+    if (active) {
 #pragma unroll 8
-    for (int j = 1; j < n; ++j) {
-      const double2 de = sde[j];
-#pragma unroll
-      for (int t = 0; t < kBisNCH; ++t) {
-        const double pn = fma(de.x + nx[t], p1[t], -de.y * p2[t]);
+      for (int j = 1; j < n; ++j) {
+        const double2 de = sde[j];
+        const double pn = fma(de.x + nx, p1, -de.y * p2);
         const int g = sgnbit(pn);
-        cnt[t] += g ^ ng[t];
-        ng[t] = g;
-        p2[t] = p1[t];
-        p1[t] = pn;
-      }
-      if ((j & 7) == 0) {
-#pragma unroll
-        for (int t = 0; t < kBisNCH; ++t) {
-          // scale both by 2^-(e - 1023), e = the larger biased exponent (exact; |e - 1023| < 1023)
-          const int ex = max(bexp(p1[t]), bexp(p2[t]));
+        cnt += g ^ ng;
+        ng = g;
+        p2 = p1;
+        p1 = pn;
+        if ((j & 7) == 0) {
+          const int ex = max(bexp(p1), bexp(p2));
           const double f = __hiloint2double((2046 - ex) << 20, 0);
-          p1[t] *= f;
-          p2[t] *= f;
+          p1 *= f;
+          p2 *= f;
         }
       }
     }
-    int m = 0;  // points with count <= i (monotone in the point index)
+    // points with count <= i (monotone in the point index 1 + kBisWpe lane + h)
+    const int mine = __popc(__ballot_sync(0xffffffffu, cnt <= i));
+    if (lane == 0) cnt_part[warp] = mine;
+    __syncthreads();
+    int m = 0;
 #pragma unroll
-    for (int t = 0; t < kBisNCH; ++t) m += __popc(__ballot_sync(0xffffffffu, cnt[t] <= i));
-    const double nlo = m >= 1 ? fma((double)m, h, lo) : lo;
-    const double nhi = m < NP ? fma((double)(m + 1), h, lo) : hi;
+    for (int q = 0; q < kBisWpe; ++q) m += cnt_part[slot * kBisWpe + q];
+    __syncthreads();
+    const double nlo = m >= 1 ? fma((double)m, hs, lo) : lo;
+    const double nhi = m < NP ? fma((double)(m + 1), hs, lo) : hi;
     lo = nlo;
     hi = fmax(nhi, nlo);
   }
-  if (lane == 0) lamall[(size_t)prob * n + i] = 0.5 * (lo + hi);
+  if (active && h == 0 && lane == 0) lamall[(size_t)prob * n + i] = 0.5 * (lo + hi);
 }
 
 // ------------------------------------------------------------------ eigenvectors of T
@@ -681,9 +683,10 @@ __global__ void __launch_bounds__(256) reflector_t_kernel(const double *__restri
   for (int j0 = k0; j0 < n; j0 += jchunk) {
     const int len = min(jchunk, n - j0);
     __syncthreads();
-    for (int t = tid; t < kNB * len; t += blockDim.x) {
-      const int r = t / len, j = j0 + t % len;
-      vs[(size_t)r * jchunk + (j - j0)] = (r < nb && j > k0 + r) ? V[(size_t)(k0 + r) * n + j] : 0.0;
+    for (int r = warp; r < kNB; r += nwarp) {  // warp per vector row, lanes along j
+      const double *src = V + (size_t)(k0 + r) * n;
+      double *dst = vs + (size_t)r * jchunk - j0;
+      for (int j = j0 + lane; j < j0 + len; j += 32) dst[j] = (r < nb && j > k0 + r) ? __ldcg(src + j) : 0.0;
     }
     __syncthreads();
     for (int pr = warp; pr < kNB * kNB; pr += nwarp) {
@@ -746,31 +749,37 @@ __global__ void __launch_bounds__(256) backtransform_kernel(const double *__rest
   }
   const int sc = tid % kBtCols, rc = tid / kBtCols;  // 256 threads: 32 x kBtCols
   // stage columns [j0, j0 + len) of the block's vectors (zero left of each vector's start)
-  auto stage = [&](int k0, int nb, int j0, int len) {
-    for (int t = tid; t < kNB * len; t += blockDim.x) {
-      const int r = t / len, j = j0 + t % len;
-      vsb[(size_t)r * jchunk + (j - j0)] = (r < nb && j > k0 + r) ? V[(size_t)(k0 + r) * n + j] : 0.0;
+  const int lane = tid & 31, warp = tid >> 5;
+  auto stage = [&](int k0, int nb, int j0, int len) {  // warp per vector row, lanes along j
+    for (int r = warp; r < kNB; r += 8) {
+      const double *src = V + (size_t)(k0 + r) * n;
+      double *dst = vsb + (size_t)r * jchunk - j0;
+      for (int j = j0 + lane; j < j0 + len; j += 32) dst[j] = (r < nb && j > k0 + r) ? __ldcg(src + j) : 0.0;
     }
   };
   for (int blk = nblk - 1; blk >= 0; --blk) {
     const int k0 = blk * kNB, nb = min(kNB, n - 2 - k0);
     for (int t = tid; t < kNB * kNB; t += blockDim.x) ts[t / kNB][t % kNB] = Tb[(size_t)blk * kNB * kNB + t];
     // W1[c][s] = v_{k0+c} . Z[:, s]
-    double a0 = 0.0, a1 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     for (int j0 = k0 + 1; j0 < n; j0 += jchunk) {
       const int len = min(jchunk, n - j0);
       __syncthreads();
       stage(k0, nb, j0, len);
       __syncthreads();
       const double *vr = vsb + (size_t)rc * jchunk;
-      int j = 0;
-      for (; j + 1 < len; j += 2) {
-        a0 = fma(vr[j], zs[(j0 + j) * kBtCols + sc], a0);
-        a1 = fma(vr[j + 1], zs[(j0 + j + 1) * kBtCols + sc], a1);
+      const double *zc = zs + (size_t)j0 * kBtCols + sc;
+      int j = max(0, k0 + rc + 1 - j0);  // v_{k0+rc} is zero before column k0 + rc + 1
+#pragma unroll 2
+      for (; j + 3 < len; j += 4) {
+        a0 = fma(vr[j], zc[j * kBtCols], a0);
+        a1 = fma(vr[j + 1], zc[(j + 1) * kBtCols], a1);
+        a2 = fma(vr[j + 2], zc[(j + 2) * kBtCols], a2);
+        a3 = fma(vr[j + 3], zc[(j + 3) * kBtCols], a3);
       }
-      if (j < len) a0 = fma(vr[j], zs[(j0 + j) * kBtCols + sc], a0);
+      for (; j < len; ++j) a0 = fma(vr[j], zc[j * kBtCols], a0);
     }
-    w1[rc][sc] = a0 + a1;
+    w1[rc][sc] = (a0 + a1) + (a2 + a3);
     __syncthreads();
     // W2 = T_b W1
     {
@@ -784,11 +793,18 @@ __global__ void __launch_bounds__(256) backtransform_kernel(const double *__rest
       __syncthreads();
       stage(k0, nb, j0, len);
       __syncthreads();
+      double w2r[kNB];
+#pragma unroll
+      for (int c = 0; c < kNB; ++c) w2r[c] = w2[c][sc];  // zero beyond nb (T_b is)
       for (int jj = rc; jj < len; jj += kNB) {
-        const int j = j0 + jj, cmax = min(nb, j - k0);
-        double acc = 0.0;
-        for (int c = 0; c < cmax; ++c) acc = fma(vsb[(size_t)c * jchunk + jj], w2[c][sc], acc);
-        zs[j * kBtCols + sc] -= acc;
+        // vsb is zero where v_{k0+c}[j] is (j <= k0 + c, c >= nb): a fixed-length sum
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < kNB; c += 2) {
+          s0 = fma(vsb[(size_t)c * jchunk + jj], w2r[c], s0);
+          s1 = fma(vsb[(size_t)(c + 1) * jchunk + jj], w2r[c + 1], s1);
+        }
+        zs[(j0 + jj) * kBtCols + sc] -= s0 + s1;
       }
     }
     __syncthreads();
@@ -1074,8 +1090,8 @@ int eig_precondition_device(double *R, int n, int *jac_gate, void *ws, size_t ws
   }
   // eigenvalues, eigenvectors of T
   {
-    const int wpb = 2;  // spread the eigenvalue warps over the SMs
-    tridiag_bisect_kernel<<<dim3((unsigned)ceil_div(n, wpb), batch), 32 * wpb, (size_t)2 * n * sizeof(double), st>>>(
+    const int wpb = 2 * kBisWpe;  // two eigenvalues per block: the warps spread over the SMs
+    tridiag_bisect_kernel<<<dim3((unsigned)ceil_div(n, wpb / kBisWpe), batch), 32 * wpb, (size_t)2 * n * sizeof(double), st>>>(
         w.d, w.e, n, w.lam);
     LRAMM_LAUNCH_CHECK();
     const int tpb = twisted_threads(n);
