@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(32 * kSytrdWarps, 1) sytrd_push_kernel(SytrdAr
   for (int li = nreg + warp; li < nl; li += nwarp) {
     const double *src = G + (int64_t)(me + (li << lgC)) * a.ldg;
     double *dst = row_ptr(li);
-    for (int j = lane; j < n; j += 32) dst[j] = src[j] * scale;
+    for (int j = lane; j < 32 * E; j += 32) dst[j] = j < n ? src[j] * scale : 0.0;
   }
   for (int j = tid; j < n; j += nth) rk[j] = G[j] * scale;
   __syncthreads();
@@ -264,10 +264,11 @@ __global__ void __launch_bounds__(32 * kSytrdWarps, 1) sytrd_push_kernel(SytrdAr
     s2 = cta_sum<32>(s2, red[1]);
     double beta, scl;
     householder(rk[1], s2, beta, tau, scl);
-    for (int j = tid; j < n; j += nth) {
-      const double vj = j < 1 ? 0.0 : (j == 1 ? 1.0 : rk[j] * scl);
+    for (int j = tid; j < ldr; j += nth) {
+      const double vj = (j < 1 || j >= n) ? 0.0 : (j == 1 ? 1.0 : rk[j] * scl);
       v[j] = vj;
-      if (me == 0 && j >= 1) Vout[j] = vj;
+      vn[j] = 0.0;
+      if (me == 0 && j >= 1 && j < n) Vout[j] = vj;
     }
     if (me == 0 && tid == 0) {
       dout[0] = rk[0];
@@ -350,11 +351,11 @@ __global__ void __launch_bounds__(32 * kSytrdWarps, 1) sytrd_push_kernel(SytrdAr
         double beta, tn, scl;
         householder_fast(alpha, s2, beta, tn, scl);
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int j = lane + 32 * e;
-          if (j < n) vn[j] = j < k + 2 ? 0.0 : (j == k + 2 ? 1.0 : rr[e] * scl);
-        }
+        for (int e = 0; e < E; ++e) vn[lane + 32 * e] = rr[e] * scl;  // zero below k+1; padded to 32 E
+        __syncwarp();
         if (lane == 0) {
+          vn[k + 1] = 0.0;
+          vn[k + 2] = 1.0;
           hh[0] = tn;
           hh[1] = dk1;
           hh[2] = beta;
@@ -405,10 +406,7 @@ __global__ void __launch_bounds__(32 * kSytrdWarps, 1) sytrd_push_kernel(SytrdAr
     }
     double vv[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int j = lane + 32 * e;
-      vv[e] = j < n ? vn[j] : 0.0;  // zero below k+2 by construction
-    }
+    for (int e = 0; e < E; ++e) vv[e] = vn[lane + 32 * e];  // zero below k+2 and beyond n
     const int ek2 = (k + 2) >> 5, lk2 = (k + 2) & 31;
     if (RM > 0 && rwi >= 0) {
       double dots[RR], cols[RR];
@@ -441,20 +439,20 @@ __global__ void __launch_bounds__(32 * kSytrdWarps, 1) sytrd_push_kernel(SytrdAr
         const int i = me + (li << lgC);
         double *ar = row_ptr(li);
         const double vi = v[i], wi = rb[i].x - c * vi;
-        double dot = 0.0, ce = 0.0;
+        // rows are padded to 32 E columns with zeros and w, v, vv vanish outside (k, n): the
+        // update and the dot run over every column without guards
+        double dot = 0.0;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
+          if (32 * e + 31 <= k) continue;  // chunk finished (warp-uniform)
           const int j = lane + 32 * e;
-          if (j > k && j < n) {
-            const double xv = fma(-wi, vr[e], fma(-vi, wr[e], ar[j]));
-            ar[j] = xv;
-            dot = fma(xv, vv[e], dot);
-            if (e == ek2) ce = xv;
-          }
+          const double xv = fma(-wi, vr[e], fma(-vi, wr[e], ar[j]));
+          ar[j] = xv;
+          dot = fma(xv, vv[e], dot);
         }
         dot = warp_allsum(dot);
-        const double ck2 = __shfl_sync(0xffffffffu, ce, lk2);
-        push(i, tn * dot, ck2, npar);
+        __syncwarp();
+        push(i, tn * dot, ar[k + 2], npar);
       }
     }
     tau = tn;
@@ -932,7 +930,7 @@ static EigPlan plan_sytrd(int n, int batch) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t budget = (size_t)optin - 4096;
-  p.ldr = (int)round_up(n, 2) + 1;
+  p.ldr = 32 * E + 1;  // rows padded to 32 E columns (odd stride)
   auto rows_per_warp = [&](int C) { return (int)ceil_div(ceil_div(n, C), nrw); };
   const int cands[5] = {1, 2, 4, 8, 16};
   int pick = 0, rm = 0;

@@ -33,5 +33,5 @@ for ev in prof.events():
     agg[nm][0] += ev.device_time; agg[nm][1] += 1
 tot = sum(v[0] for v in agg.values())
 print("sum of kernel times %.1f ms" % (tot / 1e3))
-for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:16]:
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:40]:
     print(f"{v[0]:10.0f} us {v[1]:5d}x {v[0]/v[1]:8.1f} us/launch  {k}")
