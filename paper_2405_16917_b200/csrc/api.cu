@@ -61,7 +61,7 @@ int dgemm_device(int, int64_t, int64_t, int64_t, const double *, int64_t, const 
                  void *, size_t, cudaStream_t);
 size_t dgemm_ws_bytes(int, int64_t, int64_t, int64_t);
 int qr_device(const double *, int64_t, int64_t, int64_t, double *, int64_t, double *, void *, size_t, cudaStream_t,
-              bool q_needed = true, bool fast = false);
+              bool q_needed = true, bool fast = false, const double *gram_in = nullptr);
 size_t qr_ws_bytes(int64_t, int64_t);
 int svd_tall_device(const double *, int64_t, int64_t, int64_t, double *, int64_t, double *, double *, int64_t, int *,
                     int *, void *, size_t, cudaStream_t);

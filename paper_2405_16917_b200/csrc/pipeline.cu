@@ -41,7 +41,8 @@ int dgemm_device(int trans_a, int64_t M, int64_t N, int64_t K, const double *A, 
                  int64_t ldb, double *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st);
 size_t dgemm_ws_bytes(int trans_a, int64_t M, int64_t N, int64_t K);
 int qr_device(const double *y, int64_t m, int64_t w, int64_t ldy, double *q, int64_t ldq, double *r, void *ws,
-              size_t ws_bytes, cudaStream_t st, bool q_needed = true, bool fast = false);
+              size_t ws_bytes, cudaStream_t st, bool q_needed = true, bool fast = false,
+              const double *gram_in = nullptr);
 size_t qr_ws_bytes(int64_t m, int64_t w);
 int svd_tall_pside_device(const double *T, int64_t m, int64_t n, int64_t ldt, const double *s, const double *H,
                           int64_t ldh, double *pside, int64_t ldp, int *status, void *ws, size_t ws_bytes,
@@ -82,6 +83,45 @@ __global__ void summarize_status_kernel(const int *jac_info, int njac, const int
 
 inline int elem_grid(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 8LL * num_sms())); }
 
+// ---------------------------------------------------------------- exact integer Gram
+// Per-tensor fast mode: the sketch Y = Y_int / S (S = s_x s_Omega, the qprod dequantisation, each
+// entry one correctly rounded division) carries its exact int32 accumulator: rint(Y S) recovers
+// Y_int (|Y_int| < 2^27, relative error of Y S <= 2 eps).  Y_int^T is written as 8-bit limb
+// planes, K-major (w x ldk per plane, zero padded), for the int8 tensor-core limb products
+// (igemm_limbs_device), whose exact int64 sum the epilogue divides by S^2 once: the Gram of the
+// CholeskyQR of Y, correctly rounded, from int8 products instead of an fp64 GEMM.
+__global__ void gram_limbs_kernel(const double *__restrict__ Y, int64_t rows, int w, const double *__restrict__ sa,
+                                  const double *__restrict__ sb, int nlimb, int8_t *__restrict__ planes, int64_t ldk,
+                                  int64_t plane, double *__restrict__ s_out) {
+  __shared__ int32_t t[32][33];
+  const double S = __dmul_rn(*sa, *sb);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0) *s_out = S;
+  const int64_t r0 = (int64_t)blockIdx.y * 32;
+  const int c0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {  // rows r0 + i, columns c0 + lane
+    const int64_t r = r0 + i;
+    const int c = c0 + threadIdx.x;
+    t[i][threadIdx.x] = (r < rows && c < w) ? (int32_t)rint(__dmul_rn(Y[r * w + c], S)) : 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {  // plane row c0 + i, k = r0 + lane
+    const int c = c0 + i;
+    const int64_t k = r0 + threadIdx.x;
+    if (c >= w || k >= ldk) continue;
+    int32_t v = t[threadIdx.x][i];
+    for (int l = 0; l < nlimb; ++l) {
+      int8_t d;
+      if (l == nlimb - 1) {
+        d = (int8_t)v;
+      } else {
+        d = (int8_t)(uint8_t)(v & 0xFF);
+        v = v >> 8;
+      }
+      planes[l * plane + (int64_t)c * ldk + k] = d;
+    }
+  }
+}
+
 struct QOp {  // a quantised K-major operand (bit budgets > 8: `limbs` 8-bit planes, see split_limbs)
   int8_t *q = nullptr;
   int64_t ld = 0;
@@ -107,6 +147,12 @@ struct RsvdBufs {
   double *Y = nullptr, *Q = nullptr, *Z = nullptr, *Qz = nullptr, *BsT = nullptr, *Pside = nullptr, *H = nullptr,
          *s = nullptr;
   int32_t *acc = nullptr;
+  // exact integer Gram of tall per-tensor sketches (gram_limbs_kernel)
+  int8_t *gplanes = nullptr;
+  int64_t gldk = 0;
+  int glimbs = 0;
+  int64_t *gacc = nullptr;
+  double *gram = nullptr, *gS = nullptr;
   int *info = nullptr, *compl_st = nullptr, *nonfinite = nullptr;
   void *qr_ws = nullptr, *svd_ws = nullptr, *gemm_ws = nullptr, *qz_ws = nullptr;
   void *qz_ws2 = nullptr;  // quantiser scratch of the helper stream (operand copies made off the critical path)
@@ -123,6 +169,20 @@ QOp take_qop(Arena &ar, int64_t rows, int64_t kdim, int64_t nscale, int limbs = 
   o.scale = ar.take<double>(nscale);
   o.inc = nscale > 1 ? 1 : 0;
   return o;
+}
+
+// the exact integer Gram can replace the fp64 Gram GEMM of the sketches' first CholeskyQR pass in
+// per-tensor fast mode for sketches of at least LRAMM_EXACT_GRAM_ROWS rows.  Off by default:
+// measured at c5 (131072 x 1056, 4 limbs x 4 limbs x 4 K-chunks = 64 serial int8 GEMMs with 54
+// output tiles each) the step is 78.1 ms against 67.9 ms with the fp64 DMMA Gram
+inline bool use_exact_gram(const RsvdBufs &b, const lramm_params_t &P) {
+  static const long long thr = [] {
+    const char *s = getenv("LRAMM_EXACT_GRAM_ROWS");
+    return s ? atoll(s) : 0LL;
+  }();
+  if (thr <= 0 || !b.fast || b.gran != LRAMM_GRAN_TENSOR || P.sketch_bits > 8 || P.power_bits != P.sketch_bits)
+    return false;
+  return b.rows >= thr && (double)b.cols * bit_cap(P.sketch_bits) * bit_cap(P.sketch_bits) < 2147483648.0;
 }
 
 RsvdBufs carve_rsvd(Arena &ar, int64_t rows, int64_t cols, int x_dtype, const lramm_params_t &P) {
@@ -153,6 +213,16 @@ RsvdBufs carve_rsvd(Arena &ar, int64_t rows, int64_t cols, int x_dtype, const lr
     b.qz_ws2 = ar.take<char>((int64_t)b.qz_bytes);
     int64_t mx = std::max(rows, cols);
     b.acc = ar.take<int32_t>(mx * w);
+    if (use_exact_gram(b, P)) {
+      // |Y_int| <= cols * cap_x * cap_Omega: 8-bit limbs (unsigned low bytes, signed top limb)
+      const double bound = (double)cols * bit_cap(P.sketch_bits) * bit_cap(P.sketch_bits);
+      b.glimbs = bound < 128.0 ? 1 : (bound < 32768.0 ? 2 : (bound < 8388608.0 ? 3 : 4));
+      b.gldk = round_up(rows, 16);
+      b.gplanes = ar.take<int8_t>((int64_t)b.glimbs * w * b.gldk);
+      b.gacc = ar.take<int64_t>(w * w);
+      b.gram = ar.take<double>(w * w);
+      b.gS = ar.take<double>(1);
+    }
   } else if (x_dtype == LRAMM_F32) {
     b.x64 = ar.take<double>(rows * cols);
   }
@@ -276,6 +346,26 @@ HelperStream &helper_stream(cudaStream_t main) {
   return x;
 }
 
+// G = Y^T Y exactly from the sketch's integers (per-tensor: row scale sa, column scale sb)
+int exact_gram(RsvdBufs &b, const double *Y, const double *sa, const double *sb, cudaStream_t st) {
+  const int64_t rows = b.rows, w = b.w;
+  gram_limbs_kernel<<<dim3((unsigned)ceil_div(w, 32), (unsigned)ceil_div(b.gldk, 32)), dim3(32, 8), 0, st>>>(
+      Y, rows, (int)w, sa, sb, b.glimbs, b.gplanes, b.gldk, w * b.gldk, b.gS);
+  LRAMM_LAUNCH_CHECK();
+  lramm_epilogue_t e = {};
+  e.out_dtype = LRAMM_F64;
+  e.out = b.gram;
+  e.ldo = w;
+  e.row_scale = b.gS;
+  e.row_scale_inc = 0;
+  e.col_scale = b.gS;
+  e.col_scale_inc = 0;
+  e.alpha = 1.0;
+  e.beta = 0.0;
+  return igemm_limbs_device(w, w, b.gldk, b.gplanes, b.gldk, w * b.gldk, b.glimbs, b.gplanes, b.gldk, w * b.gldk,
+                            b.glimbs, b.gacc, e, st);
+}
+
 int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, const double *omega, double *U,
              int64_t ldu, double *S, double *V, int64_t ldv, cudaStream_t st) {
   const int64_t rows = b.rows, cols = b.cols, w = b.w, r = b.r;
@@ -331,6 +421,7 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
                       st));
     LRAMM_TRY(quant(omega, LRAMM_F64, cols, w, w, P.sketch_bits, gran_r, 1, b.om, nullptr, b.qz_ws, b.qz_bytes, st));
     LRAMM_TRY(qprod(b.xr_s, b.om, rows, w, cols, b.Y, w, 0, b.acc, st));
+    if (b.gram) LRAMM_TRY(exact_gram(b, b.Y, b.xr_s.scale, b.om.scale, st));
   } else {
     if (x_dtype == LRAMM_F32) {
       f32_to_f64_kernel<<<elem_grid(rows * cols), 256, 0, st>>>((const float *)x, rows * cols, b.x64);
@@ -339,7 +430,7 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
     }
     LRAMM_TRY(dgemm_device(0, rows, w, cols, x64, cols, omega, w, b.Y, w, b.gemm_ws, b.gemm_bytes, st));
   }
-  LRAMM_TRY(qr_device(b.Y, rows, w, w, b.Q, w, nullptr, b.qr_ws, b.qr_bytes, st, true, b.fast));
+  LRAMM_TRY(qr_device(b.Y, rows, w, w, b.Q, w, nullptr, b.qr_ws, b.qr_bytes, st, true, b.fast, b.gram));
   if (b.fast && P.power_iters > 0) LRAMM_TRY(join_helper());
   for (int it = 0; it < P.power_iters; ++it) {
     // Z = X^T Q ; Qz = qr(Z) ; Y = X Qz ; Q = qr(Y)   (rsvd.py:60-64)
@@ -353,10 +444,11 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
     if (b.fast) {
       LRAMM_TRY(quant(b.Qz, LRAMM_F64, cols, w, w, P.power_bits, gran_r, 1, b.qzq, nullptr, b.qz_ws, b.qz_bytes, st));
       LRAMM_TRY(qprod(b.xr_p, b.qzq, rows, w, cols, b.Y, w, 0, b.acc, st));
+      if (b.gram) LRAMM_TRY(exact_gram(b, b.Y, b.xr_p.scale, b.qzq.scale, st));
     } else {
       LRAMM_TRY(dgemm_device(0, rows, w, cols, x64, cols, b.Qz, w, b.Y, w, b.gemm_ws, b.gemm_bytes, st));
     }
-    LRAMM_TRY(qr_device(b.Y, rows, w, w, b.Q, w, nullptr, b.qr_ws, b.qr_bytes, st, true, b.fast));
+    LRAMM_TRY(qr_device(b.Y, rows, w, w, b.Q, w, nullptr, b.qr_ws, b.qr_bytes, st, true, b.fast, b.gram));
   }
   // Bs^T = X^T Q   (rsvd.py:77, evaluated transposed)
   if (b.fast) {
