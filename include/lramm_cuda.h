@@ -243,6 +243,63 @@ int lramm_lramm(const void *a, const void *b, int in_dtype, int64_t m, int64_t k
                 size_t ws_bytes, lramm_timings_t *timings, lramm_stream_t stream);
 size_t lramm_lramm_ws(int64_t m, int64_t k, int64_t n, const lramm_params_t *params);
 
+/* ---------------------------------------------------------------- sharded pipeline (multi-GPU)
+ *
+ * One process per GPU; A is row-sharded and B column-sharded (BASELINE configs[4]).
+ * The library does not link NCCL: the caller hands it a table of collective entry points whose
+ * signatures ARE NCCL's (nccl.h ncclAllReduce / ncclAllGather, ncclResult_t returned as int,
+ * ncclDataType_t / ncclRedOp_t passed as their integer values), plus the opaque communicator
+ * they take.  A binding fills it with the addresses of ncclAllReduce / ncclAllGather and an
+ * ncclComm_t; tests fill it with host-staged callbacks.  Every collective is
+ * issued on the stream of the chain that needs it, so the call stays CUDA-graph capturable.
+ *
+ * comm_b (may be NULL): a second communicator for the rsvd chain of B, which then runs on a
+ * forked stream concurrently with A's chain (NCCL serialises the operations of ONE communicator,
+ * so two concurrent chains need two).  With comm_b == NULL and world > 1 the chains run one
+ * after the other on `stream`.  With world == 1 no collective is called (unless
+ * LRAMM_COMM_FORCE is set in flags) and the chains always run concurrently. */
+typedef int (*lramm_all_reduce_fn)(const void *sendbuff, void *recvbuff, size_t count, int nccl_dtype, int nccl_op,
+                                   void *comm, lramm_stream_t stream); /* == ncclAllReduce */
+typedef int (*lramm_all_gather_fn)(const void *sendbuff, void *recvbuff, size_t sendcount, int nccl_dtype, void *comm,
+                                   lramm_stream_t stream); /* == ncclAllGather */
+enum { LRAMM_COMM_FORCE = 1 }; /* flags: call the collectives even when world == 1 */
+typedef struct {
+  void *comm;   /* ncclComm_t of A's chain and of the recombination */
+  void *comm_b; /* ncclComm_t of B's chain, or NULL */
+  int32_t rank;
+  int32_t world;
+  int32_t flags;
+  int32_t reserved;
+  lramm_all_reduce_fn all_reduce;
+  lramm_all_gather_fn all_gather;
+} lramm_comm_t;
+
+/* Rows [lo, hi) of a dimension of `total` owned by `rank` of `world` (balanced contiguous
+ * blocks: the first total % world ranks hold one more). */
+void lramm_shard_bounds(int64_t total, int32_t world, int32_t rank, int64_t *lo, int64_t *hi);
+
+/* lramm_lramm with A row-sharded and B column-sharded over comm->world ranks (pipeline.py:159-214
+ * per rank; rsvd.py:47-94 with the exchanges below).  a_rows: this rank's rows of A,
+ * (m_hi - m_lo) x k contiguous; b_cols: this rank's columns of B, k x (n_hi - n_lo) contiguous
+ * (bounds from lramm_shard_bounds); omega_a (k x w_a) and omega_b (n x w_b) are the FULL test
+ * matrices, replicated.  c_rows / d_rows: this rank's rows of C / D, (m_hi - m_lo) x n.
+ * Exchanges, all through `comm`:
+ *   allreduce(SUM, fp64) of the w x w Gram matrices of row-sharded sketches (CholeskyQR2),
+ *   allreduce(SUM, int32) of the partial accumulators of products that contract over the sharded
+ *     dimension (A^T Q; B Omega, B Qz) -- exact, so fast-mode integers do not depend on world
+ *     (parity mode: allreduce(SUM, fp64) of the partial fp64 products),
+ *   allreduce(MAX, fp64) of quantiser absmax values that span a sharded dimension,
+ *   allgather(int8) of the quantised E2 operand before the last product.
+ * Every factor stays resident on its rank.  Restrictions: recombination bit budgets <= 8; a
+ * sketch whose Gram matrix is not numerically positive definite (rank-deficient operand) sets
+ * status = LRAMM_ERR_UNSUPPORTED (the single-GPU path's Householder fallback is not sharded). */
+int lramm_lramm_sharded(const void *a_rows, const void *b_cols, int in_dtype, int64_t m, int64_t k, int64_t n,
+                        const lramm_params_t *params, const double *omega_a, const double *omega_b,
+                        const void *c_rows, int c_dtype, void *d_rows, int d_dtype, int *status, void *ws,
+                        size_t ws_bytes, const lramm_comm_t *comm, lramm_stream_t stream);
+size_t lramm_lramm_sharded_ws(int64_t m, int64_t k, int64_t n, const lramm_params_t *params, int32_t world,
+                              int32_t rank);
+
 /* ---------------------------------------------------------------- host API */
 
 int lramm_host_matmul(const double *a, const double *b, double *out, int64_t m, int64_t k, int64_t n);

@@ -72,6 +72,27 @@ class Epilogue(ctypes.Structure):
     ]
 
 
+# lramm_comm_t: collective entry points with NCCL's own signatures (include/lramm_cuda.h)
+ALL_REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
+                                 ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p)
+ALL_GATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
+                                 ctypes.c_void_p, ctypes.c_void_p)
+COMM_FORCE = 1
+
+
+class Comm(ctypes.Structure):
+    _fields_ = [
+        ("comm", ctypes.c_void_p),
+        ("comm_b", ctypes.c_void_p),
+        ("rank", ctypes.c_int32),
+        ("world", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("all_reduce", ctypes.c_void_p),
+        ("all_gather", ctypes.c_void_p),
+    ]
+
+
 _i64, _i32, _vp, _sz, _d = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_double
 _P = ctypes.POINTER
 
@@ -108,6 +129,10 @@ SIGNATURES = {
     "lramm_lramm": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _P(Params), _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp,
                            _sz, _P(Timings), _vp]),
     "lramm_lramm_ws": (_sz, [_i64, _i64, _i64, _P(Params)]),
+    "lramm_shard_bounds": (None, [_i64, ctypes.c_int32, ctypes.c_int32, _P(_i64), _P(_i64)]),
+    "lramm_lramm_sharded": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _P(Params), _vp, _vp, _vp, _i32, _vp, _i32, _vp,
+                                   _vp, _sz, _P(Comm), _vp]),
+    "lramm_lramm_sharded_ws": (_sz, [_i64, _i64, _i64, _P(Params), ctypes.c_int32, ctypes.c_int32]),
     "lramm_host_matmul": (_i32, [_vp, _vp, _vp, _i64, _i64, _i64]),
     "lramm_host_imatmul": (_i32, [_vp, _vp, _vp, _i64, _i64, _i64]),
     "lramm_host_scale_round_clip": (_i32, [_vp, _i64, _i64, _d, _i32, _vp]),

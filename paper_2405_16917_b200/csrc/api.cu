@@ -43,10 +43,11 @@ int num_sms() {
 
 // internal entry points
 int quantize_device(const void *, int, int64_t, int64_t, int64_t, int, int, int, void *, int, int64_t, double *, int *,
-                    void *, size_t, cudaStream_t);
+                    void *, size_t, cudaStream_t, const AmaxSync *sync = nullptr);
 size_t quantize_ws_bytes(int64_t, int64_t);
 int quantize_pair_device(const void *, int, int64_t, int64_t, int64_t, int, int, int8_t *, int64_t, double *, int, int,
-                         int8_t *, int64_t, double *, int *, void *, size_t, cudaStream_t, int r_packed = 0);
+                         int8_t *, int64_t, double *, int *, void *, size_t, cudaStream_t, int r_packed = 0,
+                         const AmaxSync *sync = nullptr);
 int absmax_device(const void *, int, int64_t, int64_t, int64_t, int, double *, int *, cudaStream_t);
 int quantize_amax_device(const void *, int, int64_t, int64_t, int64_t, int, int, int, const double *, void *, int, int64_t,
                          double *, cudaStream_t);
@@ -61,16 +62,22 @@ int dgemm_device(int, int64_t, int64_t, int64_t, const double *, int64_t, const 
                  void *, size_t, cudaStream_t);
 size_t dgemm_ws_bytes(int, int64_t, int64_t, int64_t);
 int qr_device(const double *, int64_t, int64_t, int64_t, double *, int64_t, double *, void *, size_t, cudaStream_t,
-              bool q_needed = true, bool fast = false, const double *gram_in = nullptr);
+              bool q_needed = true, bool fast = false, const double *gram_in = nullptr,
+              const Coll *rows_coll = nullptr);
 size_t qr_ws_bytes(int64_t, int64_t);
 int svd_tall_device(const double *, int64_t, int64_t, int64_t, double *, int64_t, double *, double *, int64_t, int *,
-                    int *, void *, size_t, cudaStream_t);
+                    int *, void *, size_t, cudaStream_t, const Coll *rows_coll = nullptr);
 size_t svd_tall_ws_bytes(int64_t, int64_t);
 int transpose_device(const double *, int64_t, int64_t, int64_t, double *, int64_t, cudaStream_t);
 size_t rsvd_ws_bytes(int64_t, int64_t, const lramm_params_t &, int);
 int rsvd_device(const void *, int, int64_t, int64_t, const lramm_params_t &, const double *, double *, double *,
                 double *, int *, void *, size_t, cudaStream_t);
 size_t lramm_ws_bytes(int64_t, int64_t, int64_t, const lramm_params_t &, int);
+size_t lramm_sharded_ws_bytes(int64_t, int64_t, int64_t, const lramm_params_t &, int, int, int);
+void shard_bounds_host(int64_t, int, int, int64_t *, int64_t *);
+int lramm_sharded_device(const void *, const void *, int, int64_t, int64_t, int64_t, const lramm_params_t &,
+                         const double *, const double *, const void *, int, void *, int, int *, void *, size_t,
+                         const lramm_comm_t *, cudaStream_t);
 int omega_device(uint64_t key0, uint64_t key1, int64_t n, int64_t w, double *out, void *ws, size_t ws_bytes,
                  cudaStream_t st);
 size_t omega_ws_bytes(int64_t n, int64_t w);
@@ -304,6 +311,22 @@ int lramm_lramm(const void *a, const void *b, int in_dtype, int64_t m, int64_t k
   if (!params) return fail(LRAMM_ERR_PARAM, "lramm: params is NULL");
   return lramm_device(a, b, in_dtype, m, k, n, *params, omega_a, omega_b, c, c_dtype, d, d_dtype, status, ws, ws_bytes,
                       timings, (cudaStream_t)stream);
+}
+
+void lramm_shard_bounds(int64_t total, int32_t world, int32_t rank, int64_t *lo, int64_t *hi) {
+  shard_bounds_host(total, world, rank, lo, hi);
+}
+size_t lramm_lramm_sharded_ws(int64_t m, int64_t k, int64_t n, const lramm_params_t *params, int32_t world,
+                              int32_t rank) {
+  return params ? lramm_sharded_ws_bytes(m, k, n, *params, LRAMM_F32, world, rank) : 0;
+}
+int lramm_lramm_sharded(const void *a_rows, const void *b_cols, int in_dtype, int64_t m, int64_t k, int64_t n,
+                        const lramm_params_t *params, const double *omega_a, const double *omega_b,
+                        const void *c_rows, int c_dtype, void *d_rows, int d_dtype, int *status, void *ws,
+                        size_t ws_bytes, const lramm_comm_t *comm, lramm_stream_t stream) {
+  if (!params) return fail(LRAMM_ERR_PARAM, "lramm_sharded: params is NULL");
+  return lramm_sharded_device(a_rows, b_cols, in_dtype, m, k, n, *params, omega_a, omega_b, c_rows, c_dtype, d_rows,
+                              d_dtype, status, ws, ws_bytes, comm, (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------- host API

@@ -103,6 +103,41 @@ struct Arena {
   bool ok() const { return dry || off <= cap; }
 };
 
+// ------------------------------------------------------------------ collectives (sharded pipeline)
+// Thin wrapper over the caller's lramm_comm_t table (NCCL signatures and enum values,
+// include/lramm_cuda.h).  `comm` selects the communicator of the chain that issues the call.
+struct Coll {
+  const lramm_comm_t *c = nullptr;
+  void *comm = nullptr;
+  bool on() const { return c && (c->world > 1 || (c->flags & LRAMM_COMM_FORCE)); }
+  int world() const { return c ? c->world : 1; }
+  int rank() const { return c ? c->rank : 0; }
+  int reduce(void *x, size_t n, int dtype, int op, cudaStream_t st) const {
+    if (!on() || n == 0) return LRAMM_OK;
+    int rc = c->all_reduce(x, x, n, dtype, op, comm, (lramm_stream_t)st);
+    return rc ? fail(LRAMM_ERR_CUDA, "all_reduce failed with code %d", rc) : LRAMM_OK;
+  }
+  // nccl.h: ncclInt8 0, ncclInt32 2, ncclInt64 4, ncclFloat64 8; ncclSum 0, ncclMax 2
+  int sum_f64(double *x, size_t n, cudaStream_t st) const { return reduce(x, n, 8, 0, st); }
+  int max_f64(double *x, size_t n, cudaStream_t st) const { return reduce(x, n, 8, 2, st); }
+  int sum_i32(int32_t *x, size_t n, cudaStream_t st) const { return reduce(x, n, 2, 0, st); }
+  int max_i32(int32_t *x, size_t n, cudaStream_t st) const { return reduce(x, n, 2, 2, st); }
+  int gather_i8(const void *send, void *recv, size_t count, cudaStream_t st) const {
+    if (!c) return fail(LRAMM_ERR_PARAM, "all_gather without a communicator");
+    int rc = c->all_gather(send, recv, count, 0, comm, (lramm_stream_t)st);
+    return rc ? fail(LRAMM_ERR_CUDA, "all_gather failed with code %d", rc) : LRAMM_OK;
+  }
+};
+// which absmax vectors of a quantisation span a sharded dimension (allreduce(MAX) before the scales)
+struct AmaxSync {
+  const Coll *coll = nullptr;
+  bool tensor = false, row = false, col = false;  // in the INPUT's coordinates
+  bool wants(int gran) const {
+    return coll && coll->on() &&
+           (gran == LRAMM_GRAN_TENSOR ? tensor : (gran == LRAMM_GRAN_ROW ? row : col));
+  }
+};
+
 // ------------------------------------------------------------------ device numerics
 // Bit-exact conventions: every rounding step is an explicit
 // IEEE round-to-nearest intrinsic so nvcc cannot contract it into an FMA.

@@ -21,12 +21,12 @@ namespace lramm {
 
 int quantize_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits, int gran,
                     int transpose, void *q, int q_dtype, int64_t ldq, double *scales, int *nonfinite, void *ws,
-                    size_t ws_bytes, cudaStream_t st);
+                    size_t ws_bytes, cudaStream_t st, const AmaxSync *sync = nullptr);
 size_t quantize_ws_bytes(int64_t rows, int64_t cols);
 int quantize_pair_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits_r, int gran_r,
                          int8_t *qr, int64_t ldqr, double *scales_r, int bits_t, int gran_t, int8_t *qt, int64_t ldqt,
                          double *scales_t, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st,
-                         int r_packed = 0);
+                         int r_packed = 0, const AmaxSync *sync = nullptr);
 int igemm_limbs_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, int64_t pa, int la,
                        const int8_t *b, int64_t ldb, int64_t pb, int lb, int64_t *acc64,
                        const lramm_epilogue_t &epi, cudaStream_t st);
@@ -42,14 +42,16 @@ int dgemm_device(int trans_a, int64_t M, int64_t N, int64_t K, const double *A, 
 size_t dgemm_ws_bytes(int trans_a, int64_t M, int64_t N, int64_t K);
 int qr_device(const double *y, int64_t m, int64_t w, int64_t ldy, double *q, int64_t ldq, double *r, void *ws,
               size_t ws_bytes, cudaStream_t st, bool q_needed = true, bool fast = false,
-              const double *gram_in = nullptr);
+              const double *gram_in = nullptr, const Coll *rows_coll = nullptr);
 size_t qr_ws_bytes(int64_t m, int64_t w);
 int svd_tall_pside_device(const double *T, int64_t m, int64_t n, int64_t ldt, const double *s, const double *H,
                           int64_t ldh, double *pside, int64_t ldp, int *status, void *ws, size_t ws_bytes,
                           cudaStream_t st);
 int svd_tall_device(const double *T, int64_t m, int64_t n, int64_t ldt, double *pside, int64_t ldp, double *s,
-                    double *h, int64_t ldh, int *info, int *status, void *ws, size_t ws_bytes, cudaStream_t st);
+                    double *h, int64_t ldh, int *info, int *status, void *ws, size_t ws_bytes, cudaStream_t st,
+                    const Coll *rows_coll = nullptr);
 size_t svd_tall_ws_bytes(int64_t m, int64_t n);
+int qr_report_breakdown_device(void *ws, size_t ws_bytes, int64_t m, int64_t w, int *status, cudaStream_t st);
 
 namespace {
 
@@ -185,12 +187,14 @@ inline bool use_exact_gram(const RsvdBufs &b, const lramm_params_t &P) {
   return b.rows >= thr && (double)b.cols * bit_cap(P.sketch_bits) * bit_cap(P.sketch_bits) < 2147483648.0;
 }
 
-RsvdBufs carve_rsvd(Arena &ar, int64_t rows, int64_t cols, int x_dtype, const lramm_params_t &P) {
+// w_global > 0: the sketch width of the whole operand when (rows, cols) is one rank's shard
+RsvdBufs carve_rsvd(Arena &ar, int64_t rows, int64_t cols, int x_dtype, const lramm_params_t &P,
+                    int64_t w_global = 0) {
   RsvdBufs b;
   b.rows = rows;
   b.cols = cols;
   b.r = P.rank;
-  b.w = std::min<int64_t>(P.rank + P.oversample, std::min(rows, cols));
+  b.w = w_global > 0 ? w_global : std::min<int64_t>(P.rank + P.oversample, std::min(rows, cols));
   b.fast = P.mode == LRAMM_MODE_FAST;
   b.gran = P.granularity == LRAMM_GRAN_ROW ? LRAMM_GRAN_ROW : LRAMM_GRAN_TENSOR;
   const bool row = b.gran == LRAMM_GRAN_ROW;
@@ -213,7 +217,7 @@ RsvdBufs carve_rsvd(Arena &ar, int64_t rows, int64_t cols, int x_dtype, const lr
     b.qz_ws2 = ar.take<char>((int64_t)b.qz_bytes);
     int64_t mx = std::max(rows, cols);
     b.acc = ar.take<int32_t>(mx * w);
-    if (use_exact_gram(b, P)) {
+    if (w_global <= 0 && use_exact_gram(b, P)) {
       // |Y_int| <= cols * cap_x * cap_Omega: 8-bit limbs (unsigned low bytes, signed top limb)
       const double bound = (double)cols * bit_cap(P.sketch_bits) * bit_cap(P.sketch_bits);
       b.glimbs = bound < 128.0 ? 1 : (bound < 32768.0 ? 2 : (bound < 8388608.0 ? 3 : 4));
@@ -249,8 +253,11 @@ RsvdBufs carve_rsvd(Arena &ar, int64_t rows, int64_t cols, int x_dtype, const lr
 }
 
 // C (M x N fp64) = dequant(A . B^T): row scales of A, column scales of B
+// reduce (sharded pipeline): the contraction runs over a sharded dimension, so the int32
+// accumulators are partial sums; they are allreduced (exactly) before the dequantising epilogue
 int qprod(const QOp &A, const QOp &B, int64_t M, int64_t N, int64_t K, double *C, int64_t ldc, int transpose_out,
-          int32_t *acc, cudaStream_t st, int64_t *acc64 = nullptr, bool force64 = false) {
+          int32_t *acc, cudaStream_t st, int64_t *acc64 = nullptr, bool force64 = false,
+          const Coll *reduce = nullptr) {
   lramm_epilogue_t e = {};
   e.out_dtype = LRAMM_F64;
   e.transpose_out = transpose_out;
@@ -272,22 +279,28 @@ int qprod(const QOp &A, const QOp &B, int64_t M, int64_t N, int64_t K, double *C
   // split-K into at most one wave of CTAs (4096 x 272 x 4096 sketch: 64 tiles -> split 2, 4.15 -> 4.07 ms
   // c2 step against split 3's 1.3 waves)
   if (acc && tiles * 2 <= num_sms() && kb >= 8) split = (int)std::min<int64_t>(kb / 4, num_sms() / tiles);
-  if (split <= 1) return igemm_device(M, N, K, A.q, A.ld, B.q, B.ld, e, 1, st, A.packed);
-  LRAMM_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)M * N * sizeof(int32_t), st));
+  const bool red = reduce && reduce->on();
+  if (red && !acc) return fail(LRAMM_ERR_WORKSPACE, "qprod: a sharded contraction needs an int32 accumulator");
+  if (split <= 1 && !red) return igemm_device(M, N, K, A.q, A.ld, B.q, B.ld, e, 1, st, A.packed);
   lramm_epilogue_t ea = {};
   ea.out_dtype = LRAMM_I32;
-  ea.accumulate = 1;
+  ea.accumulate = split > 1 ? 1 : 0;
   ea.out = acc;
   ea.ldo = N;
-  LRAMM_TRY(igemm_device(M, N, K, A.q, A.ld, B.q, B.ld, ea, split, st, A.packed));
+  if (split > 1) LRAMM_CUDA_TRY(cudaMemsetAsync(acc, 0, (size_t)M * N * sizeof(int32_t), st));
+  LRAMM_TRY(igemm_device(M, N, K, A.q, A.ld, B.q, B.ld, ea, std::max(split, 1), st, A.packed));
+  if (red) LRAMM_TRY(reduce->sum_i32(acc, (size_t)(M * N), st));
   return epilogue_device(acc, M, N, N, e, st);
 }
 
 int quant(const void *x, int dtype, int64_t rows, int64_t cols, int64_t ldx, int bits, int gran, int transpose,
-          QOp &o, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st, int32_t *tmp32 = nullptr) {
+          QOp &o, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st, int32_t *tmp32 = nullptr,
+          const AmaxSync *sync = nullptr) {
   if (o.limbs <= 1)
     return quantize_device(x, dtype, rows, cols, ldx, bits, gran, transpose, o.q, o.packed ? LRAMM_I4 : LRAMM_I8, o.ld,
-                           o.scale, nonfinite, ws, ws_bytes, st);
+                           o.scale, nonfinite, ws, ws_bytes, st, sync);
+  if (sync && sync->coll && sync->coll->on())
+    return fail(LRAMM_ERR_UNSUPPORTED, "the sharded path carries int8 operands: bit budgets must be <= 8");
   // bit budgets > 8: the reference's integers (int32, bit-exact) -> 8-bit limb planes
   if (!tmp32) return fail(LRAMM_ERR_WORKSPACE, "quant: multi-limb operand needs an int32 staging buffer");
   const int64_t orows = transpose ? cols : rows, kdim = transpose ? rows : cols;
@@ -366,9 +379,35 @@ int exact_gram(RsvdBufs &b, const double *Y, const double *sa, const double *sb,
                             b.glimbs, b.gacc, e, st);
 }
 
+// How one operand of the sharded pipeline is split: A by rows, B by columns.
+struct ShardSpec {
+  Coll coll;                     // the communicator of this operand's chain
+  int kind = 0;                  // 0 whole operand, 1 rows of X sharded, 2 columns of X sharded
+  int64_t g_rows = 0, g_cols = 0;  // global shape of X (accumulator guards)
+};
+
+// sh (sharded pipeline): x holds this rank's rows (kind 1) or columns (kind 2) of X and b is carved
+// for that local shape with the global sketch width; omega = the rows of Omega that meet the local
+// columns.  Products that contract over the sharded dimension allreduce their partial sums
+// (int32 accumulators in fast mode: exact), the QRs of row-sharded sketches allreduce their
+// Gram matrices, and quantiser maxima that span the sharded dimension are allreduced (MAX).
+// Outputs: kind 1 -> U local rows, V replicated; kind 2 -> U replicated, V local rows.
 int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, const double *omega, double *U,
-             int64_t ldu, double *S, double *V, int64_t ldv, cudaStream_t st) {
+             int64_t ldu, double *S, double *V, int64_t ldv, cudaStream_t st, const ShardSpec *sh = nullptr) {
   const int64_t rows = b.rows, cols = b.cols, w = b.w, r = b.r;
+  const int kind = sh ? sh->kind : 0;
+  const Coll *coll = sh ? &sh->coll : nullptr;
+  const bool coll_on = coll && coll->on();
+  const Coll *red_rows = kind == 1 ? coll : nullptr;  // contraction over X's rows is partial
+  const Coll *red_cols = kind == 2 ? coll : nullptr;  // contraction over X's columns is partial
+  const Coll *qr_rows = kind == 1 ? coll : nullptr;   // rows x w sketches are row-sharded
+  const Coll *qr_cols = kind == 2 ? coll : nullptr;   // cols x w sketches are row-sharded
+  // absmax vectors that span the sharded dimension (input coordinates of each quantisation)
+  const AmaxSync sync_x{coll, kind != 0, kind == 2, kind == 1};  // X itself
+  const AmaxSync sync_tall{coll, true, false, true};             // a row-sharded rows x w / cols x w matrix
+  const AmaxSync *sx = kind ? &sync_x : nullptr;
+  const AmaxSync *s_rows = kind == 1 ? &sync_tall : nullptr;  // Q (rows x w)
+  const AmaxSync *s_cols = kind == 2 ? &sync_tall : nullptr;  // Omega_j, Qz (cols x w)
   LRAMM_CUDA_TRY(cudaMemsetAsync(b.info, 0, 4 * sizeof(int), st));
   LRAMM_CUDA_TRY(cudaMemsetAsync(b.compl_st, 0, 4 * sizeof(int), st));
   LRAMM_CUDA_TRY(cudaMemsetAsync(b.nonfinite, 0, 4 * sizeof(int), st));
@@ -387,21 +426,29 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
   const bool need_xc_p = b.fast && P.power_iters > 0 && !pair;
   const bool need_xc_j = b.fast && (b.xc_j.q != b.xc_p.q || P.power_iters == 0) && !(pair && P.power_iters == 0);
   if (need_xp_row || need_xc_p || need_xc_j) {
-    // the remaining X-only operand copies on the helper stream (joined before their first use)
-    hs = &helper_stream(st);
-    LRAMM_CUDA_TRY(cudaEventRecord(hs->fork, st));
-    LRAMM_CUDA_TRY(cudaStreamWaitEvent(hs->st, hs->fork, 0));
+    // the remaining X-only operand copies on the helper stream (joined before their first use);
+    // with live collectives they stay on the chain's stream: one communicator, one stream
+    cudaStream_t hst = st;
+    if (!coll_on) {
+      hs = &helper_stream(st);
+      LRAMM_CUDA_TRY(cudaEventRecord(hs->fork, st));
+      LRAMM_CUDA_TRY(cudaStreamWaitEvent(hs->st, hs->fork, 0));
+      hst = hs->st;
+    }
+    void *hws = coll_on ? b.qz_ws : b.qz_ws2;
     if (need_xp_row)
-      LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.power_bits, gran_l, 0, b.xr_p, b.nonfinite, b.qz_ws2, b.qz_bytes,
-                      hs->st));
+      LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.power_bits, gran_l, 0, b.xr_p, b.nonfinite, hws, b.qz_bytes, hst,
+                      nullptr, sx));
     if (need_xc_p)
-      LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.power_bits, gran_c, 1, b.xc_p, b.nonfinite, b.qz_ws2, b.qz_bytes,
-                      hs->st));
+      LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.power_bits, gran_c, 1, b.xc_p, b.nonfinite, hws, b.qz_bytes, hst,
+                      nullptr, sx));
     if (need_xc_j)
-      LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.proj_bits, gran_c, 1, b.xc_j, b.nonfinite, b.qz_ws2, b.qz_bytes,
-                      hs->st));
-    LRAMM_CUDA_TRY(cudaEventRecord(hs->join, hs->st));
-    helper = true;
+      LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.proj_bits, gran_c, 1, b.xc_j, b.nonfinite, hws, b.qz_bytes, hst,
+                      nullptr, sx));
+    if (!coll_on) {
+      LRAMM_CUDA_TRY(cudaEventRecord(hs->join, hs->st));
+      helper = true;
+    }
   }
   auto join_helper = [&]() -> int {
     if (helper) {
@@ -410,17 +457,24 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
     }
     return LRAMM_OK;
   };
+  // thin QR of a sketch; row-sharded sketches report a Cholesky breakdown (no sharded fallback)
+  auto qr = [&](const double *y, int64_t m, double *q, const Coll *rc, const double *gram_in) -> int {
+    LRAMM_TRY(qr_device(y, m, w, w, q, w, nullptr, b.qr_ws, b.qr_bytes, st, true, b.fast, gram_in, rc));
+    if (rc) LRAMM_TRY(qr_report_breakdown_device(b.qr_ws, b.qr_bytes, m, w, b.compl_st, st));
+    return LRAMM_OK;
+  };
   if (b.fast) {
     // Y = X . Omega at sketch_bits
     if (pair)
       LRAMM_TRY(quantize_pair_device(x, x_dtype, rows, cols, cols, P.sketch_bits, gran_l, b.xr_s.q, b.xr_s.ld,
                                      b.xr_s.scale, bits_first, gran_c, xc_first.q, xc_first.ld, xc_first.scale,
-                                     b.nonfinite, b.qz_ws, b.qz_bytes, st, b.xr_s.packed));
+                                     b.nonfinite, b.qz_ws, b.qz_bytes, st, b.xr_s.packed, sx));
     else
       LRAMM_TRY(quant(x, x_dtype, rows, cols, cols, P.sketch_bits, gran_l, 0, b.xr_s, b.nonfinite, b.qz_ws, b.qz_bytes,
-                      st));
-    LRAMM_TRY(quant(omega, LRAMM_F64, cols, w, w, P.sketch_bits, gran_r, 1, b.om, nullptr, b.qz_ws, b.qz_bytes, st));
-    LRAMM_TRY(qprod(b.xr_s, b.om, rows, w, cols, b.Y, w, 0, b.acc, st));
+                      st, nullptr, sx));
+    LRAMM_TRY(quant(omega, LRAMM_F64, cols, w, w, P.sketch_bits, gran_r, 1, b.om, nullptr, b.qz_ws, b.qz_bytes, st,
+                    nullptr, s_cols));
+    LRAMM_TRY(qprod(b.xr_s, b.om, rows, w, cols, b.Y, w, 0, b.acc, st, nullptr, false, red_cols));
     if (b.gram) LRAMM_TRY(exact_gram(b, b.Y, b.xr_s.scale, b.om.scale, st));
   } else {
     if (x_dtype == LRAMM_F32) {
@@ -429,38 +483,45 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
       x64 = b.x64;
     }
     LRAMM_TRY(dgemm_device(0, rows, w, cols, x64, cols, omega, w, b.Y, w, b.gemm_ws, b.gemm_bytes, st));
+    if (red_cols) LRAMM_TRY(red_cols->sum_f64(b.Y, (size_t)(rows * w), st));
   }
-  LRAMM_TRY(qr_device(b.Y, rows, w, w, b.Q, w, nullptr, b.qr_ws, b.qr_bytes, st, true, b.fast, b.gram));
+  LRAMM_TRY(qr(b.Y, rows, b.Q, qr_rows, b.gram));
   if (b.fast && P.power_iters > 0) LRAMM_TRY(join_helper());
   for (int it = 0; it < P.power_iters; ++it) {
     // Z = X^T Q ; Qz = qr(Z) ; Y = X Qz ; Q = qr(Y)   (rsvd.py:60-64)
     if (b.fast) {
-      LRAMM_TRY(quant(b.Q, LRAMM_F64, rows, w, w, P.power_bits, gran_r, 1, b.qq, nullptr, b.qz_ws, b.qz_bytes, st));
-      LRAMM_TRY(qprod(b.xc_p, b.qq, cols, w, rows, b.Z, w, 0, b.acc, st));
+      LRAMM_TRY(quant(b.Q, LRAMM_F64, rows, w, w, P.power_bits, gran_r, 1, b.qq, nullptr, b.qz_ws, b.qz_bytes, st,
+                      nullptr, s_rows));
+      LRAMM_TRY(qprod(b.xc_p, b.qq, cols, w, rows, b.Z, w, 0, b.acc, st, nullptr, false, red_rows));
     } else {
       LRAMM_TRY(dgemm_device(1, cols, w, rows, x64, cols, b.Q, w, b.Z, w, b.gemm_ws, b.gemm_bytes, st));
+      if (red_rows) LRAMM_TRY(red_rows->sum_f64(b.Z, (size_t)(cols * w), st));
     }
-    LRAMM_TRY(qr_device(b.Z, cols, w, w, b.Qz, w, nullptr, b.qr_ws, b.qr_bytes, st, true, b.fast));
+    LRAMM_TRY(qr(b.Z, cols, b.Qz, qr_cols, nullptr));
     if (b.fast) {
-      LRAMM_TRY(quant(b.Qz, LRAMM_F64, cols, w, w, P.power_bits, gran_r, 1, b.qzq, nullptr, b.qz_ws, b.qz_bytes, st));
-      LRAMM_TRY(qprod(b.xr_p, b.qzq, rows, w, cols, b.Y, w, 0, b.acc, st));
+      LRAMM_TRY(quant(b.Qz, LRAMM_F64, cols, w, w, P.power_bits, gran_r, 1, b.qzq, nullptr, b.qz_ws, b.qz_bytes, st,
+                      nullptr, s_cols));
+      LRAMM_TRY(qprod(b.xr_p, b.qzq, rows, w, cols, b.Y, w, 0, b.acc, st, nullptr, false, red_cols));
       if (b.gram) LRAMM_TRY(exact_gram(b, b.Y, b.xr_p.scale, b.qzq.scale, st));
     } else {
       LRAMM_TRY(dgemm_device(0, rows, w, cols, x64, cols, b.Qz, w, b.Y, w, b.gemm_ws, b.gemm_bytes, st));
+      if (red_cols) LRAMM_TRY(red_cols->sum_f64(b.Y, (size_t)(rows * w), st));
     }
-    LRAMM_TRY(qr_device(b.Y, rows, w, w, b.Q, w, nullptr, b.qr_ws, b.qr_bytes, st, true, b.fast, b.gram));
+    LRAMM_TRY(qr(b.Y, rows, b.Q, qr_rows, b.gram));
   }
   // Bs^T = X^T Q   (rsvd.py:77, evaluated transposed)
   if (b.fast) {
     LRAMM_TRY(join_helper());
-    LRAMM_TRY(quant(b.Q, LRAMM_F64, rows, w, w, P.proj_bits, gran_r, 1, b.qq, nullptr, b.qz_ws, b.qz_bytes, st));
-    LRAMM_TRY(qprod(b.xc_j, b.qq, cols, w, rows, b.BsT, w, 0, b.acc, st));
+    LRAMM_TRY(quant(b.Q, LRAMM_F64, rows, w, w, P.proj_bits, gran_r, 1, b.qq, nullptr, b.qz_ws, b.qz_bytes, st, nullptr,
+                    s_rows));
+    LRAMM_TRY(qprod(b.xc_j, b.qq, cols, w, rows, b.BsT, w, 0, b.acc, st, nullptr, false, red_rows));
   } else {
     LRAMM_TRY(dgemm_device(1, cols, w, rows, x64, cols, b.Q, w, b.BsT, w, b.gemm_ws, b.gemm_bytes, st));
+    if (red_rows) LRAMM_TRY(red_rows->sum_f64(b.BsT, (size_t)(cols * w), st));
   }
   // SVD(Bs): u = H, v = Bs^T H diag(s)^-1   (rsvd.py:78, _jacobi.py)
   LRAMM_TRY(svd_tall_device(b.BsT, cols, w, w, nullptr, w, b.s, b.H, w, b.info, b.compl_st, b.svd_ws, b.svd_bytes,
-                             st));
+                             st, qr_cols));
   // v = Bs^T H diag(s)^-1 on the helper stream, concurrent with the lift U = Q u (rsvd.py:79-81);
   // both then truncated to r (rsvd.py:84-94)
   HelperStream &hv = helper_stream(st);
@@ -717,6 +778,225 @@ int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t 
     for (int i = 0; i < 6; ++i) cudaEventDestroy(ev[i]);
   }
   return LRAMM_OK;
+}
+
+// ------------------------------------------------------------------ sharded pipeline (multi-GPU)
+namespace {
+
+void shard_bounds(int64_t total, int world, int rank, int64_t &lo, int64_t &hi) {
+  const int64_t base = total / world, extra = total % world;
+  lo = rank * base + std::min<int64_t>(rank, extra);
+  hi = lo + base + (rank < extra ? 1 : 0);
+}
+
+struct ShardedBufs {
+  RsvdBufs ra, rb;
+  double *UA, *SA, *VA, *UB, *SB, *VB, *E1, *Zsc, *E2T, *Usc;
+  QOp vt, wq, e1q, zq, e2q, uq;
+  int8_t *gath = nullptr, *e2all = nullptr;  // allgathered int8 E2 rows (padded per rank) / compacted
+  int64_t n_pad = 0;
+  int32_t *acc;
+  int *nonfinite, *st_loc;
+  void *qws;
+  size_t qbytes;
+};
+
+ShardedBufs carve_sharded(Arena &ar, int64_t ml, int64_t k, int64_t nl, int64_t m, int64_t n, int in_dtype,
+                          const lramm_params_t &P, int world) {
+  ShardedBufs L;
+  const int64_t r = P.rank;
+  const int64_t wa = std::min<int64_t>(P.rank + P.oversample, std::min(m, k));
+  const int64_t wb = std::min<int64_t>(P.rank + P.oversample, std::min(k, n));
+  L.ra = carve_rsvd(ar, ml, k, in_dtype, P, wa);
+  L.rb = carve_rsvd(ar, k, nl, in_dtype, P, wb);
+  L.UA = ar.take<double>(ml * r);
+  L.SA = ar.take<double>(r);
+  L.VA = ar.take<double>(k * r);
+  L.UB = ar.take<double>(k * r);
+  L.SB = ar.take<double>(r);
+  L.VB = ar.take<double>(nl * r);
+  L.E1 = ar.take<double>(r * r);
+  L.Zsc = ar.take<double>(nl * r);
+  L.E2T = ar.take<double>(nl * r);
+  L.Usc = ar.take<double>(ml * r);
+  L.vt = take_qop(ar, r, k, 1);
+  L.wq = take_qop(ar, r, k, 1);
+  L.e1q = take_qop(ar, r, r, 1);
+  L.zq = take_qop(ar, nl, r, 1);
+  L.n_pad = ceil_div(n, world);
+  L.e2q = take_qop(ar, L.n_pad, r, 1);  // this rank's rows, zero-padded to the largest shard
+  L.uq = take_qop(ar, ml, r, 1);
+  L.gath = ar.take<int8_t>((int64_t)world * L.n_pad * L.e2q.ld);
+  L.e2all = ar.take<int8_t>(n * L.e2q.ld);
+  L.acc = ar.take<int32_t>(std::max(r * r, r * nl));
+  L.nonfinite = ar.take<int>(4);
+  L.st_loc = ar.take<int>(4);
+  const int64_t mx = std::max(std::max(ml, nl), std::max(k, r));
+  L.qbytes = quantize_ws_bytes(mx, mx);
+  L.qws = ar.take<char>((int64_t)L.qbytes);
+  return L;
+}
+
+// this rank's status: a Jacobi non-convergence, a non-finite input, or a chain's own code
+// (LRAMM_ERR_UNSUPPORTED for a sketch without a sharded fallback)
+__global__ void sharded_status_kernel(const int *ia, const int *ib, const int *ca, const int *cb, const int *nfa,
+                                      const int *nfb, const int *nf, int *status) {
+  if (threadIdx.x) return;
+  int s = 0;
+  if (ia[0] < 0 || ib[0] < 0) s = LRAMM_ERR_NONCONVERGENCE;
+  if (!s && ca[0]) s = ca[0];
+  if (!s && cb[0]) s = cb[0];
+  if (nfa[0] || nfb[0] || nf[0]) s = LRAMM_ERR_NONFINITE;
+  *status = s;
+}
+
+}  // namespace
+
+size_t lramm_sharded_ws_bytes(int64_t m, int64_t k, int64_t n, const lramm_params_t &P, int in_dtype, int world,
+                              int rank) {
+  if (world < 1 || rank < 0 || rank >= world) return 0;
+  int64_t m0, m1, n0, n1;
+  shard_bounds(m, world, rank, m0, m1);
+  shard_bounds(n, world, rank, n0, n1);
+  Arena ar;
+  ar.dry = true;
+  carve_sharded(ar, std::max<int64_t>(m1 - m0, 1), k, std::max<int64_t>(n1 - n0, 1), m, n, in_dtype, P, world);
+  return ar.off + 1024;
+}
+
+void shard_bounds_host(int64_t total, int world, int rank, int64_t *lo, int64_t *hi) {
+  int64_t a = 0, b = 0;
+  if (world >= 1 && rank >= 0 && rank < world) shard_bounds(total, world, rank, a, b);
+  if (lo) *lo = a;
+  if (hi) *hi = b;
+}
+
+int lramm_sharded_device(const void *a_rows, const void *b_cols, int in_dtype, int64_t m, int64_t k, int64_t n,
+                         const lramm_params_t &P, const double *omega_a, const double *omega_b, const void *c_rows,
+                         int c_dtype, void *d_rows, int d_dtype, int *status, void *ws, size_t ws_bytes,
+                         const lramm_comm_t *comm, cudaStream_t st) {
+  LRAMM_TRY(validate_params(P, true));
+  if (!comm || comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world)
+    return fail(LRAMM_ERR_PARAM, "lramm_sharded: bad communicator (rank / world)");
+  const int world = comm->world, rank = comm->rank;
+  const bool live = world > 1 || (comm->flags & LRAMM_COMM_FORCE);
+  if (live && (!comm->all_reduce || !comm->all_gather))
+    return fail(LRAMM_ERR_PARAM, "lramm_sharded: the communicator has no all_reduce / all_gather entry point");
+  if (P.rank < 2) return fail(LRAMM_ERR_PARAM, "rank must be >= 2, got %d", P.rank);
+  if (in_dtype != LRAMM_F32 && in_dtype != LRAMM_F64) return fail(LRAMM_ERR_PARAM, "inputs must be F32 or F64");
+  if (d_dtype != LRAMM_F32 && d_dtype != LRAMM_F64) return fail(LRAMM_ERR_PARAM, "output must be F32 or F64");
+  if (m < 1 || k < 1 || n < 1) return fail(LRAMM_ERR_SHAPE, "empty operand");
+  if (P.rank > std::min(m, k) || P.rank > std::min(k, n))
+    return fail(LRAMM_ERR_PARAM, "rank %d exceeds operand min dims %lld, %lld", P.rank, (long long)std::min(m, k),
+                (long long)std::min(k, n));
+  if (m < world || n < world)
+    return fail(LRAMM_ERR_SHAPE, "lramm_sharded: every rank needs at least one row of A and one column of B");
+  const int64_t r = P.rank;
+  const int d1 = P.bits[0], d2 = P.bits[1], d3 = P.bits[2];
+  if (std::max(d1, std::max(d2, d3)) > 8)
+    return fail(LRAMM_ERR_UNSUPPORTED, "the sharded path carries int8 operands: recombination bit budgets must be <= 8");
+  // int32 accumulators are summed across the ranks: guard with the GLOBAL contraction lengths
+  LRAMM_TRY(check_acc(k, d1, d1));
+  LRAMM_TRY(check_acc(r, d2, d2));
+  LRAMM_TRY(check_acc(r, d3, d3));
+  if (P.mode == LRAMM_MODE_FAST) {
+    const int64_t mx = std::max(std::max(m, n), k);
+    LRAMM_TRY(check_acc(mx, P.sketch_bits, P.sketch_bits));
+    LRAMM_TRY(check_acc(mx, P.proj_bits, P.proj_bits));
+    if (P.power_iters > 0) LRAMM_TRY(check_acc(mx, P.power_bits, P.power_bits));
+  }
+  int64_t m0, m1, n0, n1;
+  shard_bounds(m, world, rank, m0, m1);
+  shard_bounds(n, world, rank, n0, n1);
+  const int64_t ml = m1 - m0, nl = n1 - n0;
+  Arena ar(ws, ws_bytes);
+  ShardedBufs L = carve_sharded(ar, ml, k, nl, m, n, in_dtype, P, world);
+  if (!ar.ok()) return fail(LRAMM_ERR_WORKSPACE, "lramm_sharded: workspace too small (%zu needed)", ar.off);
+
+  ShardSpec sa, sb;
+  sa.coll = Coll{comm, comm->comm};
+  sa.kind = 1;
+  sa.g_rows = m;
+  sa.g_cols = k;
+  sb.coll = Coll{comm, comm->comm_b ? comm->comm_b : comm->comm};
+  sb.kind = 2;
+  sb.g_rows = k;
+  sb.g_cols = n;
+  const Coll &coll = sa.coll;
+  const double *omega_bj = omega_b + n0 * L.rb.w;  // the rows of Omega_B that meet this rank's columns
+  // ---- rsvd of both operands: concurrent chains unless they would share one live communicator
+  const bool fork = !live || comm->comm_b != nullptr;
+  if (fork) {
+    SideStream &side = side_stream(st);
+    LRAMM_CUDA_TRY(cudaEventRecord(side.fork, st));
+    LRAMM_CUDA_TRY(cudaStreamWaitEvent(side.st, side.fork, 0));
+    LRAMM_TRY(run_rsvd(b_cols, in_dtype, L.rb, P, omega_bj, L.UB, r, L.SB, L.VB, r, side.st, &sb));
+    LRAMM_TRY(run_rsvd(a_rows, in_dtype, L.ra, P, omega_a, L.UA, r, L.SA, L.VA, r, st, &sa));
+    LRAMM_CUDA_TRY(cudaEventRecord(side.join, side.st));
+    LRAMM_CUDA_TRY(cudaStreamWaitEvent(st, side.join, 0));
+  } else {
+    LRAMM_TRY(run_rsvd(a_rows, in_dtype, L.ra, P, omega_a, L.UA, r, L.SA, L.VA, r, st, &sa));
+    LRAMM_TRY(run_rsvd(b_cols, in_dtype, L.rb, P, omega_bj, L.UB, r, L.SB, L.VB, r, st, &sb));
+  }
+  // ---- scaling (pipeline.py:188-193) of the local rows: Usc = U_A sigma_A, Zsc^T = V_B sigma_B
+  scale_cols_kernel<<<elem_grid(ml * r), 256, 0, st>>>(L.UA, ml, (int)r, r, L.SA, L.Usc, r);
+  LRAMM_LAUNCH_CHECK();
+  scale_cols_kernel<<<elem_grid(nl * r), 256, 0, st>>>(L.VB, nl, (int)r, r, L.SB, L.Zsc, r);
+  LRAMM_LAUNCH_CHECK();
+  LRAMM_CUDA_TRY(cudaMemsetAsync(L.nonfinite, 0, 4 * sizeof(int), st));
+  const AmaxSync global_t{&coll, true, false, false};  // per-tensor scale of a sharded matrix
+  // ---- E1 = QM(V_A^T U_B, d1): both operands replicated, computed on every rank (r x r, K = k)
+  LRAMM_TRY(quant(L.VA, LRAMM_F64, k, r, r, d1, LRAMM_GRAN_TENSOR, 1, L.vt, L.nonfinite, L.qws, L.qbytes, st));
+  LRAMM_TRY(quant(L.UB, LRAMM_F64, k, r, r, d1, LRAMM_GRAN_TENSOR, 1, L.wq, L.nonfinite, L.qws, L.qbytes, st));
+  LRAMM_TRY(qprod(L.vt, L.wq, r, r, k, L.E1, r, 0, L.acc, st));
+  // ---- E2 = QM(E1 Zsc, d2): the local rows of E2^T (n_j x r, K = r), Zsc's scale made global
+  LRAMM_TRY(quant(L.E1, LRAMM_F64, r, r, r, d2, LRAMM_GRAN_TENSOR, 0, L.e1q, L.nonfinite, L.qws, L.qbytes, st));
+  LRAMM_TRY(quant(L.Zsc, LRAMM_F64, nl, r, r, d2, LRAMM_GRAN_TENSOR, 0, L.zq, L.nonfinite, L.qws, L.qbytes, st, nullptr,
+                  &global_t));
+  LRAMM_TRY(qprod(L.e1q, L.zq, r, nl, r, L.E2T, r, 1, nullptr, st));
+  // ---- E3 = QM(Usc E2, d3); D rows = alpha E3 + beta C rows (m_i x n, K = r): E2's int8 rows are
+  // allgathered (rank j's rows at j * n_pad), then compacted when the shards are ragged
+  LRAMM_TRY(quant(L.Usc, LRAMM_F64, ml, r, r, d3, LRAMM_GRAN_TENSOR, 0, L.uq, L.nonfinite, L.qws, L.qbytes, st, nullptr,
+                  &global_t));
+  if (coll.on() && nl < L.n_pad)
+    LRAMM_CUDA_TRY(cudaMemsetAsync(L.e2q.q + nl * L.e2q.ld, 0, (size_t)((L.n_pad - nl) * L.e2q.ld), st));
+  LRAMM_TRY(quant(L.E2T, LRAMM_F64, nl, r, r, d3, LRAMM_GRAN_TENSOR, 0, L.e2q, L.nonfinite, L.qws, L.qbytes, st, nullptr,
+                  &global_t));
+  const int8_t *e2 = L.e2q.q;
+  if (coll.on()) {
+    LRAMM_TRY(coll.gather_i8(L.e2q.q, L.gath, (size_t)(L.n_pad * L.e2q.ld), st));
+    if (n % world == 0) {
+      e2 = L.gath;
+    } else {
+      for (int j = 0; j < world; ++j) {
+        int64_t lo, hi;
+        shard_bounds(n, world, j, lo, hi);
+        LRAMM_CUDA_TRY(cudaMemcpyAsync(L.e2all + lo * L.e2q.ld, L.gath + (int64_t)j * L.n_pad * L.e2q.ld,
+                                       (size_t)((hi - lo) * L.e2q.ld), cudaMemcpyDeviceToDevice, st));
+      }
+      e2 = L.e2all;
+    }
+  }
+  {
+    lramm_epilogue_t e = {};
+    e.out_dtype = d_dtype;
+    e.out = d_rows;
+    e.ldo = n;
+    e.row_scale = L.uq.scale;
+    e.row_scale_inc = 0;
+    e.col_scale = L.e2q.scale;
+    e.col_scale_inc = 0;
+    e.alpha = P.alpha;
+    e.beta = c_rows ? P.beta : 0.0;
+    e.c = c_rows;
+    e.c_dtype = c_dtype;
+    e.ldc = n;
+    LRAMM_TRY(igemm_device(ml, n, r, L.uq.q, L.uq.ld, e2, L.e2q.ld, e, 1, st));
+  }
+  sharded_status_kernel<<<1, 32, 0, st>>>(L.ra.info, L.rb.info, L.ra.compl_st, L.rb.compl_st, L.ra.nonfinite,
+                                          L.rb.nonfinite, L.nonfinite, status);
+  LRAMM_LAUNCH_CHECK();
+  return coll.max_i32(status, 1, st);  // every rank reports the same status
 }
 
 }  // namespace lramm

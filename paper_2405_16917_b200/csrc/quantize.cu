@@ -610,20 +610,22 @@ int quantize_from_amax(const T *x, int64_t rows, int64_t cols, int64_t ldx, int 
 template <class T>
 int quantize_impl(const T *x, int64_t rows, int64_t cols, int64_t ldx, int bits, int gran, int transpose,
                   void *q, int q_dtype, int64_t ldq, double *scales, int *nonfinite, void *ws,
-                  size_t ws_bytes, cudaStream_t st) {
+                  size_t ws_bytes, cudaStream_t st, const AmaxSync *sync) {
   const int64_t nscale = gran == LRAMM_GRAN_TENSOR ? 1 : (gran == LRAMM_GRAN_ROW ? rows : cols);
   Arena ar(ws, ws_bytes);
   double *amax = ar.take<double>(nscale);
   if (!ar.ok() || amax == nullptr) return fail(LRAMM_ERR_WORKSPACE, "quantize: workspace too small");
   LRAMM_CUDA_TRY(cudaMemsetAsync(amax, 0, nscale * sizeof(double), st));
   LRAMM_TRY(absmax_launch<T>(x, rows, cols, ldx, gran, amax, nonfinite, st));
+  if (sync && sync->wants(gran)) LRAMM_TRY(sync->coll->max_f64(amax, (size_t)nscale, st));
   return quantize_from_amax<T>(x, rows, cols, ldx, bits, gran, transpose, amax, q, q_dtype, ldq, scales, false, st);
 }
 
 template <class T>
 int quantize_pair_impl(const T *x, int64_t rows, int64_t cols, int64_t ldx, int bits_r, int gran_r, int8_t *qr,
                        int64_t ldqr, double *scales_r, int bits_t, int gran_t, int8_t *qt, int64_t ldqt,
-                       double *scales_t, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st, int r_packed) {
+                       double *scales_t, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st, int r_packed,
+                       const AmaxSync *sync) {
   Arena ar(ws, ws_bytes);
   const bool need[3] = {gran_r == LRAMM_GRAN_TENSOR || gran_t == LRAMM_GRAN_TENSOR,
                         gran_r == LRAMM_GRAN_ROW || gran_t == LRAMM_GRAN_ROW,
@@ -638,6 +640,8 @@ int quantize_pair_impl(const T *x, int64_t rows, int64_t cols, int64_t ldx, int 
     if (need[g]) amax[g] = base + off, off += (int)round_up(n[g], 32);
   LRAMM_CUDA_TRY(cudaMemsetAsync(base, 0, total * sizeof(double), st));
   LRAMM_TRY(absmax_tile_launch<T>(x, rows, cols, ldx, amax[0], amax[1], amax[2], nonfinite, st));
+  for (int g = 0; g < 3; ++g)  // maxima over a sharded dimension: combined across the ranks
+    if (need[g] && sync && sync->wants(g)) LRAMM_TRY(sync->coll->max_f64(amax[g], (size_t)n[g], st));
   const int cap_r = bit_cap(bits_r), cap_t = bit_cap(bits_t);
   QSide R{qr, ldqr, scales_r, gran_r, cap_r, r_packed, amax[gran_r]}, Tq{qt, ldqt, scales_t, gran_t, cap_t, 0, amax[gran_t]};
   const bool r_ok = r_packed ? (ldqr % 2 == 0 && (uintptr_t)qr % 2 == 0) : tile_ok(R);
@@ -655,7 +659,7 @@ int quantize_pair_impl(const T *x, int64_t rows, int64_t cols, int64_t ldx, int 
 
 int quantize_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits,
                     int gran, int transpose, void *q, int q_dtype, int64_t ldq, double *scales,
-                    int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st) {
+                    int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st, const AmaxSync *sync) {
   if (rows < 1 || cols < 1 || ldx < cols) return fail(LRAMM_ERR_SHAPE, "quantize: bad shape %lldx%lld ld %lld",
                                                       (long long)rows, (long long)cols, (long long)ldx);
   if (bits < 2 || bits > 24) return fail(LRAMM_ERR_PARAM, "bits must be an integer in [2, 24], got %d", bits);
@@ -667,10 +671,10 @@ int quantize_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int6
   if (gran < 0 || gran > 2) return fail(LRAMM_ERR_PARAM, "bad granularity %d", gran);
   if (x_dtype == LRAMM_F32)
     return quantize_impl<float>((const float *)x, rows, cols, ldx, bits, gran, transpose, q, q_dtype, ldq,
-                                scales, nonfinite, ws, ws_bytes, st);
+                                scales, nonfinite, ws, ws_bytes, st, sync);
   if (x_dtype == LRAMM_F64)
     return quantize_impl<double>((const double *)x, rows, cols, ldx, bits, gran, transpose, q, q_dtype, ldq,
-                                 scales, nonfinite, ws, ws_bytes, st);
+                                 scales, nonfinite, ws, ws_bytes, st, sync);
   return fail(LRAMM_ERR_PARAM, "quantize: input dtype must be F32 or F64");
 }
 
@@ -702,7 +706,8 @@ int quantize_amax_device(const void *x, int x_dtype, int64_t rows, int64_t cols,
 // gran_t; gran in input coordinates) from a single absmax pass and a single read of x
 int quantize_pair_device(const void *x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx, int bits_r, int gran_r,
                          int8_t *qr, int64_t ldqr, double *scales_r, int bits_t, int gran_t, int8_t *qt, int64_t ldqt,
-                         double *scales_t, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st, int r_packed) {
+                         double *scales_t, int *nonfinite, void *ws, size_t ws_bytes, cudaStream_t st, int r_packed,
+                         const AmaxSync *sync) {
   if (rows < 1 || cols < 1 || ldx < cols) return fail(LRAMM_ERR_SHAPE, "quantize: bad shape");
   if (bits_r < 2 || bits_r > 8 || bits_t < 2 || bits_t > 8)
     return fail(LRAMM_ERR_UNSUPPORTED, "quantize pair: int8 outputs need bits in [2, 8]");
@@ -711,10 +716,10 @@ int quantize_pair_device(const void *x, int x_dtype, int64_t rows, int64_t cols,
   if ((r_packed ? 2 * ldqr : ldqr) < cols || ldqt < rows) return fail(LRAMM_ERR_SHAPE, "quantize pair: ldq too small");
   if (x_dtype == LRAMM_F32)
     return quantize_pair_impl<float>((const float *)x, rows, cols, ldx, bits_r, gran_r, qr, ldqr, scales_r, bits_t,
-                                     gran_t, qt, ldqt, scales_t, nonfinite, ws, ws_bytes, st, r_packed);
+                                     gran_t, qt, ldqt, scales_t, nonfinite, ws, ws_bytes, st, r_packed, sync);
   if (x_dtype == LRAMM_F64)
     return quantize_pair_impl<double>((const double *)x, rows, cols, ldx, bits_r, gran_r, qr, ldqr, scales_r, bits_t,
-                                      gran_t, qt, ldqt, scales_t, nonfinite, ws, ws_bytes, st, r_packed);
+                                      gran_t, qt, ldqt, scales_t, nonfinite, ws, ws_bytes, st, r_packed, sync);
   return fail(LRAMM_ERR_PARAM, "quantize: input dtype must be F32 or F64");
 }
 

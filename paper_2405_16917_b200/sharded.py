@@ -14,9 +14,20 @@ only these exchanges cross NVLink (torch.distributed / NCCL):
   * allgather of the int8 E2 operand (r x n) before the last product; D stays
     row-sharded.
 
-The orchestration is written against two small interfaces so the same code is
-exercised on one B200 (`CudaOps`, the C ABI) and, in the test-suite, with the gloo
-backend on CPU against the oracle (`tests/test_sharded_cpu.py` supplies NumPy ops).
+Two implementations of the same algorithm:
+
+  * `lramm_sharded_native` -> the C-ABI entry `lramm_lramm_sharded` (csrc/pipeline.cu): the whole
+    sharded pipeline as one stream-ordered, CUDA-graph-capturable call.  The library does not
+    link NCCL; it receives a table of collective entry points with NCCL's signatures
+    (`lramm_comm_t`).  `NcclComm` fills it with torch's own libnccl (ncclAllReduce /
+    ncclAllGather and two communicators created with ncclCommInitRank, one per rsvd chain so
+    the A and B chains run concurrently); `HostStagedComm` fills it with callbacks that stage
+    through the host and a torch.distributed (gloo) group -- for tests where several ranks
+    share one GPU, which NCCL refuses.
+  * `lramm_sharded` -> the op-by-op orchestration below, written against two small interfaces
+    (`Comm`, ops) so the same code runs on one B200 (`CudaOps`, the C ABI) and, in the
+    test-suite, with the gloo backend on CPU against the oracle (`tests/test_sharded_cpu.py`
+    supplies NumPy ops).  It is the executable specification of the native path.
 """
 
 from __future__ import annotations
@@ -70,6 +81,198 @@ class Comm:
         parts = [torch.empty_like(pad) for _ in range(self.world)]
         self.dist.all_gather(parts, pad, group=self.group)
         return torch.cat([p[: int(s.item())] for p, s in zip(parts, sizes)], dim=0)
+
+
+# ------------------------------------------------------------------ native path (lramm_lramm_sharded)
+
+_NCCL_DTYPE_TORCH = {0: torch.int8, 2: torch.int32, 4: torch.int64, 8: torch.float64}  # nccl.h ncclDataType_t
+_NCCL_SUM, _NCCL_MAX = 0, 2  # nccl.h ncclRedOp_t
+
+
+def _load_nccl():
+    """torch's own libnccl (already mapped by libtorch_cuda; resolved by its SONAME)."""
+    import glob
+    import os
+    import site
+
+    try:
+        return ctypes.CDLL("libnccl.so.2")
+    except OSError:
+        pass
+    for base in site.getsitepackages() + [os.path.dirname(os.path.dirname(torch.__file__))]:
+        for cand in glob.glob(os.path.join(base, "nvidia", "nccl", "lib", "libnccl.so*")):
+            return ctypes.CDLL(cand)
+    raise RuntimeError("libnccl.so.2 not found (torch.distributed's NCCL backend ships it)")
+
+
+def _load_cudart():
+    """The CUDA runtime torch already mapped (host-staged test collectives copy through it)."""
+    import glob
+    import os
+    import site
+
+    for name in ("libcudart.so.12", "libcudart.so"):
+        try:
+            return ctypes.CDLL(name)
+        except OSError:
+            pass
+    for base in site.getsitepackages() + ["/usr/local/cuda/lib64"]:
+        for cand in glob.glob(os.path.join(base, "nvidia", "cuda_runtime", "lib", "libcudart.so*")) + glob.glob(
+                os.path.join(base, "libcudart.so*")):
+            return ctypes.CDLL(cand)
+    raise RuntimeError("libcudart not found")
+
+
+class _NcclUniqueId(ctypes.Structure):
+    _fields_ = [("internal", ctypes.c_char * 128)]  # nccl.h NCCL_UNIQUE_ID_BYTES
+
+
+class NcclComm:
+    """lramm_comm_t over NCCL: the table holds the addresses of ncclAllReduce / ncclAllGather and
+    two ncclComm_t (A's chain + recombination, B's chain) created on the current CUDA device.
+    The unique ids travel through the already initialised torch.distributed group (any backend).
+    force=True calls the collectives even at world size 1 (plumbing test on one GPU)."""
+
+    def __init__(self, group=None, force=False, two_comms=True):
+        import torch.distributed as dist
+
+        self.lib = _load_nccl()
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.lib.ncclGetUniqueId.argtypes = [ctypes.POINTER(_NcclUniqueId)]
+        self.lib.ncclCommInitRank.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, _NcclUniqueId, ctypes.c_int]
+        self.lib.ncclCommDestroy.argtypes = [ctypes.c_void_p]
+        self.comms = []
+        for _ in range(2 if two_comms else 1):
+            uid = _NcclUniqueId()
+            if self.rank == 0:
+                rc = self.lib.ncclGetUniqueId(ctypes.byref(uid))
+                if rc:
+                    raise RuntimeError(f"ncclGetUniqueId failed: {rc}")
+            if self.world > 1:
+                box = [bytes(uid.internal) if self.rank == 0 else None]
+                dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                           group=group)
+                ctypes.memmove(ctypes.byref(uid), box[0], 128)
+            comm = ctypes.c_void_p()
+            rc = self.lib.ncclCommInitRank(ctypes.byref(comm), self.world, uid, self.rank)
+            if rc:
+                raise RuntimeError(f"ncclCommInitRank failed: {rc}")
+            self.comms.append(comm)
+        self.table = N.Comm()
+        self.table.comm = self.comms[0]
+        self.table.comm_b = self.comms[1] if two_comms else None
+        self.table.rank, self.table.world = self.rank, self.world
+        self.table.flags = N.COMM_FORCE if force else 0
+        self.table.all_reduce = ctypes.cast(self.lib.ncclAllReduce, ctypes.c_void_p)
+        self.table.all_gather = ctypes.cast(self.lib.ncclAllGather, ctypes.c_void_p)
+
+    def close(self):
+        for c in self.comms:
+            self.lib.ncclCommDestroy(c)
+        self.comms = []
+
+
+class HostStagedComm:
+    """lramm_comm_t whose collectives stage through the host and a torch.distributed group (gloo):
+    synchronous, not graph-capturable -- for tests where the ranks share one GPU."""
+
+    def __init__(self, group=None, force=False):
+        import torch.distributed as dist
+
+        self.dist, self.group = dist, group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.rt = _load_cudart()
+        self.calls = {"all_reduce": 0, "all_gather": 0, "bytes": 0}
+
+        def _to_host(src, count, code, stream):
+            t = torch.empty(count, dtype=_NCCL_DTYPE_TORCH[code])
+            torch.cuda.synchronize()
+            _memcpy(t.data_ptr(), src, t.numel() * t.element_size())
+            return t
+
+        def _memcpy(dst, src, nbytes):
+            if self.rt.cudaMemcpy(ctypes.c_void_p(dst), ctypes.c_void_p(src), ctypes.c_size_t(nbytes), 4):  # Default
+                raise RuntimeError("cudaMemcpy failed")
+
+        def all_reduce(send, recv, count, code, op, comm, stream):
+            try:
+                t = _to_host(send, count, code, stream)
+                if self.world > 1:
+                    dist.all_reduce(t, op=dist.ReduceOp.SUM if op == _NCCL_SUM else dist.ReduceOp.MAX, group=group)
+                _memcpy(recv, t.data_ptr(), t.numel() * t.element_size())
+                self.calls["all_reduce"] += 1
+                self.calls["bytes"] += t.numel() * t.element_size()
+                return 0
+            except Exception:  # noqa: BLE001 -- a C callback must not raise
+                return 1
+
+        def all_gather(send, recv, count, code, comm, stream):
+            try:
+                t = _to_host(send, count, code, stream)
+                parts = [torch.empty_like(t) for _ in range(self.world)]
+                if self.world > 1:
+                    dist.all_gather(parts, t, group=group)
+                else:
+                    parts = [t]
+                full = torch.cat(parts)
+                _memcpy(recv, full.data_ptr(), full.numel() * full.element_size())
+                self.calls["all_gather"] += 1
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        self._ar, self._ag = N.ALL_REDUCE_FN(all_reduce), N.ALL_GATHER_FN(all_gather)  # keep alive
+        self.table = N.Comm()
+        self.table.comm = None
+        self.table.comm_b = None  # one host-side group: the chains run one after the other
+        self.table.rank, self.table.world = self.rank, self.world
+        self.table.flags = N.COMM_FORCE if force else 0
+        self.table.all_reduce = ctypes.cast(self._ar, ctypes.c_void_p)
+        self.table.all_gather = ctypes.cast(self._ag, ctypes.c_void_p)
+
+    def close(self):
+        pass
+
+
+def lramm_sharded_native(a_rows, b_cols, shape, params, comm, c_rows=None, out=None):
+    """This rank's rows of D = alpha * A @ B + beta * C through the C-ABI `lramm_lramm_sharded`
+    (one stream-ordered call; CUDA-graph capturable with an `NcclComm`).
+
+    a_rows: (m_i x k) CUDA tensor, b_cols: (k x n_j) CUDA tensor (bounds: `shard_bounds`);
+    shape = (m, k, n); comm: `NcclComm` or `HostStagedComm`.  Returns (d_rows, status) with
+    status a device int32 tensor (0 = ok, identical on every rank)."""
+    from .pipeline import _params
+    from ._device import dtype_code
+
+    m, k, n = shape
+    dev = a_rows.device
+    (ma, mb), (na, nb) = shard_bounds(m, n, comm.world, comm.rank)
+    if tuple(a_rows.shape) != (mb - ma, k) or tuple(b_cols.shape) != (k, nb - na):
+        from .errors import ShapeError
+
+        raise ShapeError(f"rank {comm.rank}: expected shards {(mb - ma, k)} and {(k, nb - na)}, got "
+                         f"{tuple(a_rows.shape)} and {tuple(b_cols.shape)}")
+    if a_rows.dtype != b_cols.dtype:
+        a_rows, b_cols = a_rows.double(), b_cols.double()
+    a_rows, b_cols = a_rows.contiguous(), b_cols.contiguous()
+    seed_a, seed_b = _child_seeds(params.seed)
+    om_a = OMEGA.device_omega(seed_a, k, sketch_width((m, k), params.rank, params.oversample), dev)
+    om_b = OMEGA.device_omega(seed_b, n, sketch_width((k, n), params.rank, params.oversample), dev)
+    p = _params(params)
+    out_t = torch.float64 if np.dtype(params.out_dtype) == np.float64 else torch.float32
+    if out is None:
+        out = torch.empty((mb - ma, n), dtype=out_t, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    wsz = N.LIB.lramm_lramm_sharded_ws(m, k, n, ctypes.byref(p), comm.world, comm.rank)
+    ws = WORKSPACE.get(wsz, dev)
+    cc = c_rows.contiguous() if (c_rows is not None and params.beta != 0.0) else None
+    N.check(N.LIB.lramm_lramm_sharded(ptr(a_rows), ptr(b_cols), dtype_code(a_rows), m, k, n, ctypes.byref(p), ptr(om_a),
+                                      ptr(om_b), ptr(cc), dtype_code(cc) if cc is not None else N.F64, ptr(out),
+                                      dtype_code(out), ptr(status), ptr(ws), wsz, ctypes.byref(comm.table),
+                                      stream_handle(dev)))
+    return out, status
 
 
 class CudaOps:
