@@ -202,13 +202,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-accuracy", action="store_true", help="skip the report-only accuracy checks")
     ap.add_argument("--sharded", action="store_true",
-                    help="run the row/column-sharded path (default for c5 at N > 1) even at N = 1")
+                    help="run the row/column-sharded path (the default at N > 1 for a single pair) even at N = 1")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: one independent pair per rank (no collective) instead of the sharded pair")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, cfg, world, rank)
-    if args.sharded or (cfg.get("sharded") and world > 1):
+    # N > 1: a single pair is row/column-sharded over the ranks (north_star (4)); the batched
+    # config shards its pairs instead; --replicas runs one independent pair per rank
+    if args.sharded or (world > 1 and cfg.get("pairs", 1) == 1 and not args.replicas):
         return run_sharded(args, cfg, world, rank, local)
     return run_ours(args, cfg, world, rank, local)
 
@@ -230,7 +234,7 @@ def workload_config(cfg, args, world):
     total = cfg.get("pairs", 1)
     which = {"c1": "configs[0]", "c2": "configs[1]", "c3": "configs[2]", "c4": "configs[3]",
              "c5": "configs[4]"}[args.config]
-    sharded = cfg.get("sharded") and world > 1
+    sharded = world > 1 and total == 1 and not getattr(args, "replicas", False)
     return {"workload": f"BASELINE {which}: {total} x {cfg['m']}x{cfg['k']}x{cfg['n']} fp32 {spectrum_name(cfg)} "
                         f"spectrum, r={cfg['rank']} p={cfg['oversample']} q={cfg['power_iters']}, "
                         f"int{cfg['sketch_bits']}/int{cfg['power_bits']}/int{cfg['proj_bits']} "
@@ -527,7 +531,11 @@ def run_ours(args, cfg, world, rank, local):
 
 def run_sharded(args, cfg, world, rank, local):
     """One approximate GEMM per step with A row-sharded and B column-sharded over the ranks
-    (SURVEY §8(e)); value = 2mnk / (max-over-ranks device time), strong scaling."""
+     through the C-ABI entry lramm_lramm_sharded: NCCL allreduces of the Gram
+    matrices, the int32 partial accumulators and the quantiser maxima, one int8 allgather; the
+    whole step captured in a CUDA graph.  value = 2mnk / (max-over-ranks device time), strong
+    scaling.  At N = 1 (--sharded) the collectives still go through NCCL (single-rank
+    communicators) so the line measures the same code path."""
     import torch
 
     torch.cuda.set_device(local)
@@ -537,7 +545,7 @@ def run_sharded(args, cfg, world, rank, local):
 
         dist.init_process_group("nccl", device_id=dev)
     import paper_2405_16917_b200 as L
-    from paper_2405_16917_b200.sharded import Comm, CudaOps, lramm_sharded, shard_bounds
+    from paper_2405_16917_b200.sharded import NcclComm, lramm_sharded_native, shard_bounds
 
     m, k, n = cfg["m"], cfg["k"], cfg["n"]
     a, b = synth_pair(cfg, 0, dev)  # same seed on every rank: each keeps its own slice
@@ -545,18 +553,50 @@ def run_sharded(args, cfg, world, rank, local):
     a_i, b_j = a[ma:mb].contiguous(), b[:, na:nb].contiguous()
     del a, b
     torch.cuda.empty_cache()
-    params = L.LrammParams(rank=cfg["rank"], bits=tuple(cfg["bits"]), power_iters=cfg["power_iters"],
-                           oversample=cfg["oversample"], seed=0, mode=cfg["mode"], sketch_bits=cfg["sketch_bits"],
-                           power_bits=cfg["power_bits"], proj_bits=cfg["proj_bits"], granularity=cfg["granularity"])
-    comm, ops = Comm(), CudaOps(local)
+    kw = dict(rank=cfg["rank"], bits=tuple(cfg["bits"]), power_iters=cfg["power_iters"], oversample=cfg["oversample"],
+              seed=0, mode=cfg["mode"], sketch_bits=cfg["sketch_bits"], power_bits=cfg["power_bits"],
+              proj_bits=cfg["proj_bits"], granularity=cfg["granularity"])
+    params = L.LrammParams(out_dtype=np.float32, **kw)
+    # two communicators let the A and B chains run concurrently; across ranks that is only safe when
+    # NCCL's kernels and ours can always be co-resident, so the default at N > 1 is one communicator
+    # (chains one after the other); SHARDED_TWO_COMMS=1 opts in
+    two = world == 1 or os.environ.get("SHARDED_TWO_COMMS", "0") == "1"
+    # NCCL prints its version banner on stdout at communicator creation: keep stdout for the JSON line
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        comm = NcclComm(force=(world == 1), two_comms=two)
+        torch.cuda.synchronize()
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
+    out = torch.empty((mb - ma, n), dtype=torch.float32, device=dev)
 
     def step():
-        return lramm_sharded(a_i, b_j, (m, k, n), params, comm=comm, ops=ops)
+        return lramm_sharded_native(a_i, b_j, (m, k, n), params, comm, out=out)
 
     clocks = ClockSampler(local).__enter__()
     time.sleep(0.5)
+    for _ in range(max(1, args.warmup)):
+        _d, status = step()
+    torch.cuda.synchronize()
+    st = int(status.item())
+    if st:
+        raise RuntimeError(f"lramm_sharded status {st}")
+    # capture one step (kernels + NCCL collectives) into a CUDA graph
+    cap = torch.cuda.Stream(device=dev)
+    cap.wait_stream(torch.cuda.current_stream(dev))
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(cap):
+        step()  # sizes this stream's workspace
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=cap):
+            step()
+    torch.cuda.synchronize()
     for _ in range(max(3, args.warmup)):
-        step()
+        graph.replay()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -565,34 +605,46 @@ def run_sharded(args, cfg, world, rank, local):
     torch.cuda.synchronize()
     e0.record()
     for _ in range(args.steps):
-        step()
+        graph.replay()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    t_end = time.time() + 1.0
+    while time.time() < t_end:  # keep the GPU loaded for the clock sampler (untimed)
+        graph.replay()
+        torch.cuda.synchronize()
     clocks.__exit__(None, None, None)
     clock_summary = clocks.summary(clk_mark)
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
+        torch.distributed.barrier()
     ms_per_step = ms / args.steps
     value = effective_ops(cfg) / (ms_per_step * 1e-3) / 1e12
 
-    # e2e: this rank's shards from pinned host memory, D rows back to the host, every step
+    # e2e: this rank's shards from pinned host memory, its fp64 D rows back to the host, every step
+    p64 = L.LrammParams(**kw)
     ha = torch.empty(a_i.shape, dtype=torch.float32, pin_memory=True)
     hb = torch.empty(b_j.shape, dtype=torch.float32, pin_memory=True)
     ha.copy_(a_i)
     hb.copy_(b_j)
     hd = torch.empty((mb - ma, n), dtype=torch.float64, pin_memory=True)
+    d64 = torch.empty((mb - ma, n), dtype=torch.float64, device=dev)
     e2e_steps = max(1, min(args.steps, 3))
+
+    def e2e_step():
+        da, db = ha.to(dev, non_blocking=True), hb.to(dev, non_blocking=True)
+        lramm_sharded_native(da, db, (m, k, n), p64, comm, out=d64)
+        hd.copy_(d64)
+
+    e2e_step()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        da, db = ha.to(dev, non_blocking=True), hb.to(dev, non_blocking=True)
-        d = lramm_sharded(da, db, (m, k, n), params, comm=comm, ops=ops)
-        hd.copy_(d)
+        e2e_step()
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     if world > 1:
@@ -601,23 +653,34 @@ def run_sharded(args, cfg, world, rank, local):
         e2e_s = float(t.item())
     e2e = {"value": effective_ops(cfg) / e2e_s / 1e12, "unit": "TOPS",
            "h2d_bytes_per_step": 4 * (a_i.numel() + b_j.numel()), "d2h_bytes_per_step": 8 * hd.numel(),
-           "ms_per_step": e2e_s * 1e3, "path": "sharded lramm on this rank's pinned host shards, fp64 D rows"}
-    top_name, top_us, top_per_step, step_us, launches, _ = roofline_probe(L, None, None, None, reps=2, step=step)
-    roof = dominant_roofline(top_name, top_us, cfg, measured_peaks())
+           "ms_per_step": e2e_s * 1e3,
+           "path": "lramm_sharded_native (C ABI lramm_lramm_sharded) on this rank's pinned host shards, fp64 D rows"}
+    top_name, top_us, top_per_step, step_us, launches, per = roofline_probe(L, None, None, None, reps=2, step=step)
+    peaks = measured_peaks()
+    if rank == 0:
+        peaks["live"] = measure_peaks(dev)
+    roof = dominant_roofline(top_name, top_us, cfg, peaks)
     roof.update(kernel=top_name, us_per_launch=top_us, launches_per_step=top_per_step,
                 share_of_step=top_us * top_per_step / step_us if step_us else None)
+    nccl = [(us, c) for name, (us, c) in per.items() if "nccl" in name.lower()] if per else []
+    nccl_us = sum(us for us, _c in nccl) / 2 if per else None
+    launches -= sum(c for _us, c in nccl) // 2  # gpu_launches counts this library's kernels only
     line = {"metric": "effective approx-GEMM TOPS (2mnk/time)", "value": value, "unit": "TOPS", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
-            "dtype": "int8 x int8 -> int32 (tcgen05) sketch/QM GEMMs; fp64 factorisation; fp64 D",
+            "dtype": "int8 x int8 -> int32 (tcgen05) sketch/QM GEMMs; fp64 factorisation; fp32 D",
             "data": "synthetic (SURVEY §8(d) spectrum, Haar factors from seeded torch QR)",
             "config": dict(workload_config(cfg, args, world), parallelism=(
-                f"{world} ranks, A row-sharded / B column-sharded, Gram + int32 partial allreduces, E2 allgather"
-                if world > 1 else "sharded code path at world size 1 (no collectives)")),
+                f"{world} ranks, A row-sharded / B column-sharded (lramm_lramm_sharded): NCCL allreduce of Gram "
+                f"matrices, int32 partial accumulators and quantiser maxima, int8 E2 allgather; "
+                f"{'two communicators, concurrent A/B chains' if two else 'one communicator, A then B chain'}; "
+                f"one CUDA graph per step" + ("" if world > 1 else "; single-rank NCCL communicators"))),
             "clocks": clock_summary, "e2e": e2e, "gpu_launches": launches * args.steps,
-            "gpu_launches_per_step": launches, "roofline": roof}
+            "gpu_launches_per_step": launches, "roofline": roof, "nccl_us_per_step": nccl_us,
+            "peaks": peaks.get("live")}
     if rank == 0:
         print(json.dumps(line))
+    comm.close()
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0

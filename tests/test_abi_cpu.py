@@ -48,6 +48,9 @@ def test_struct_layouts_match_header():
     assert N.Params.alpha.offset == 24 and N.Params.mode.offset == 40
     assert ctypes.sizeof(N.Epilogue) == 96
     assert ctypes.sizeof(N.Timings) == 20
+    # lramm_comm_t: two communicators, rank/world/flags/reserved, two function pointers
+    assert ctypes.sizeof(N.Comm) == 48
+    assert N.Comm.rank.offset == 16 and N.Comm.all_reduce.offset == 32 and N.Comm.all_gather.offset == 40
 
 
 def test_params_validation_mirrors_reference():
@@ -162,3 +165,41 @@ def test_omega_key_and_ziggurat_tables_reproduce_numpy():
     ref = np.random.Generator(np.random.Philox(np.random.SeedSequence([77, 0x534B, 40, 9]))).standard_normal(40000)
     assert np.array_equal(np.array(out), ref)
     assert np.array_equal(O.gaussian_sketch(77, 40, 9).ravel(), ref[:360])  # the oracle's Omega is this stream
+
+
+def test_shard_bounds_match_the_python_split():
+    """lramm_shard_bounds (the C ABI's balanced contiguous split) == sharded.shard_bounds."""
+    from paper_2405_16917_b200 import _native as N
+    from paper_2405_16917_b200.sharded import _row_split
+
+    for total in (1, 7, 8, 449, 8192, 131072):
+        for world in (1, 2, 3, 4, 8):
+            offs = _row_split(total, world)
+            for rank in range(world):
+                lo, hi = ctypes.c_int64(), ctypes.c_int64()
+                N.LIB.lramm_shard_bounds(total, world, rank, ctypes.byref(lo), ctypes.byref(hi))
+                assert (lo.value, hi.value) == (offs[rank], offs[rank + 1])
+
+
+def test_sharded_entry_validates_before_touching_the_device():
+    from paper_2405_16917_b200 import _native as N
+    from paper_2405_16917_b200.pipeline import LrammParams, _params
+
+    p = _params(LrammParams(rank=8))
+    args = lambda comm: (None, None, N.F64, 64, 64, 64, ctypes.byref(p), None, None, None, N.F64, None, N.F64,  # noqa: E731
+                         None, None, 0, comm, None)
+    assert N.LIB.lramm_lramm_sharded(*args(None)) == N.ERR_PARAM
+    comm = N.Comm()
+    comm.rank, comm.world = 2, 2  # rank out of range
+    assert N.LIB.lramm_lramm_sharded(*args(ctypes.byref(comm))) == N.ERR_PARAM
+    comm.rank, comm.world = 0, 2  # live communicator without entry points
+    assert N.LIB.lramm_lramm_sharded(*args(ctypes.byref(comm))) == N.ERR_PARAM
+    assert b"all_reduce" in N.LIB.lramm_last_error()
+    wide = _params(LrammParams(rank=8, bits=(16, 8, 8)))
+    one = N.Comm()
+    one.rank, one.world = 0, 1
+    a = list(args(ctypes.byref(one)))
+    a[6] = ctypes.byref(wide)
+    assert N.LIB.lramm_lramm_sharded(*a) == N.ERR_UNSUPPORTED
+    assert N.LIB.lramm_lramm_sharded_ws(4096, 4096, 4096, ctypes.byref(p), 2, 0) < \
+        N.LIB.lramm_lramm_ws(4096, 4096, 4096, ctypes.byref(p))
