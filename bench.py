@@ -242,7 +242,8 @@ def workload_config(cfg, args, world):
             "name": args.config, "m": cfg["m"], "k": cfg["k"], "n": cfg["n"], "rank": cfg["rank"],
             "oversample": cfg["oversample"], "power_iters": cfg["power_iters"], "bits": list(cfg["bits"]),
             "mode": cfg["mode"], "granularity": cfg["granularity"], "pairs_per_rank": pairs_per_rank(cfg, world),
-            "streams": min(pairs_per_rank(cfg, world), cfg.get("streams", 1)),
+            "streams": min(pairs_per_rank(cfg, world), int(os.environ.get("BENCH_STREAMS", cfg.get("streams", 1)))),
+            "graphs": max(1, min(pairs_per_rank(cfg, world), int(os.environ.get("BENCH_GRAPHS", cfg.get("graphs", 1))))),
             "parallelism": (f"{world} ranks, A row-sharded / B column-sharded, NCCL Gram + int32 partial "
                             f"allreduces, E2 allgather" if sharded else
                             f"{world} ranks, independent pairs sharded across ranks (no collective)" if world > 1
@@ -409,16 +410,53 @@ def run_ours(args, cfg, world, rank, local):
     st = int(status.item())
     if st:
         raise RuntimeError(f"lramm status {st}")
-    # capture one step (all pairs of this rank) into a CUDA graph
-    cap = torch.cuda.Stream(device=dev)
-    cap.wait_stream(torch.cuda.current_stream(dev))
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(cap):
-        issue_all()
-        torch.cuda.synchronize()
-        with torch.cuda.graph(graph, stream=cap):
-            issue_all()
+    # capture one step (all pairs of this rank) into a CUDA graph -- or, for the batched config, into
+    # BENCH_GRAPHS graphs (pairs split evenly) replayed side by side on their own launch streams
+    G = max(1, min(P, int(os.environ.get("BENCH_GRAPHS", cfg.get("graphs", 1)))))
+    groups = [list(range(g, P, G)) for g in range(G)]
+
+    def issue_group(g):
+        cur = torch.cuda.current_stream(dev)
+        mine = streams[g::G] if S >= G else [streams[g % S]]
+        for st_ in mine:
+            st_.wait_stream(cur)
+        for i, j in enumerate(groups[g]):
+            with torch.cuda.stream(mine[i % len(mine)]):
+                L.lramm_device(pairs[j][0], pairs[j][1], params, out=outs[j])
+        for st_ in mine:
+            cur.wait_stream(st_)
+
+    caps = [torch.cuda.Stream(device=dev) for _ in range(G)]
+    graphs = [torch.cuda.CUDAGraph() for _ in range(G)]
+    for g in range(G):
+        caps[g].wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(caps[g]):
+            if G == 1:
+                issue_all()
+            else:
+                issue_group(g)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graphs[g], stream=caps[g]):
+                if G == 1:
+                    issue_all()
+                else:
+                    issue_group(g)
     torch.cuda.synchronize()
+
+    class _Replay:
+        def replay(self):
+            if G == 1:
+                graphs[0].replay()
+                return
+            cur = torch.cuda.current_stream(dev)
+            for g in range(G):
+                caps[g].wait_stream(cur)
+                with torch.cuda.stream(caps[g]):
+                    graphs[g].replay()
+            for g in range(G):
+                cur.wait_stream(caps[g])
+
+    graph = _Replay()
     for _ in range(args.warmup):
         graph.replay()
     torch.cuda.synchronize()
@@ -462,7 +500,12 @@ def run_ours(args, cfg, world, rank, local):
     # P > 1 (batched pairs): the pairs are issued from a pool of host threads, each call on its own
     # leased C-ABI context and streams (the reference's sweeps use a thread pool the same way,
     # cli.py:415-419); per-thread pinned D buffers
-    workers = min(P, 8)
+    # P == 1: INFLIGHT calls are kept in flight from as many host threads, so call i+1's upload and
+    # call i-1's download overlap call i's factorisation (PCIe is full duplex and each call leases its
+    # own context); every call still moves its own A, B up and its own D down inside the timed region.
+    # The latency of one isolated call is reported next to the throughput.
+    inflight = max(1, int(os.environ.get("BENCH_E2E_INFLIGHT", 3)))
+    workers = min(P, 8) if P > 1 else inflight
     tls = threading.local()
 
     def host_call(pair):
@@ -474,13 +517,22 @@ def run_ours(args, cfg, world, rank, local):
     from concurrent.futures import ThreadPoolExecutor
 
     pool = ThreadPoolExecutor(max_workers=workers)
+    calls = host_pairs if P > 1 else host_pairs * (inflight * int(os.environ.get("BENCH_E2E_ROUNDS", 6)))
     for _ in range(max(1, min(args.warmup, 2))):
-        list(pool.map(host_call, host_pairs[:workers]))
+        list(pool.map(host_call, (host_pairs * workers)[:workers]))
     e2e_steps = max(1, min(args.steps, 5 if P == 1 else 1))
+    lat_s = None
+    if P == 1:  # one isolated call at a time
+        host_call(host_pairs[0])  # this thread's pinned D buffer
+        t0 = time.perf_counter()
+        for _ in range(3):
+            host_call(host_pairs[0])
+        lat_s = (time.perf_counter() - t0) / 3
+        e2e_steps = 1
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        list(pool.map(host_call, host_pairs))
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
+        list(pool.map(host_call, calls))
+    e2e_s = (time.perf_counter() - t0) / e2e_steps / (len(calls) // P)
     pool.shutdown()
     if world > 1:
         t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
@@ -494,7 +546,13 @@ def run_ours(args, cfg, world, rank, local):
            "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
            "path": "lramm(numpy) -> lramm_host_lramm (C ABI), pinned A/B/D, fp64 D like the reference; "
                    "Omega from the device generator (cached per seed)"
-                   + (f"; pairs issued from {workers} host threads" if P > 1 else "")}
+                   + (f"; pairs issued from {workers} host threads" if P > 1 else
+                      f"; {len(calls)} calls, {inflight} in flight from {inflight} host threads (throughput); "
+                      "single_call_ms = one isolated call")}
+    if lat_s is not None:
+        e2e["single_call_ms"] = lat_s * 1e3
+        e2e["single_call_value"] = effective_ops(cfg) * world / lat_s / 1e12
+        e2e["calls_in_flight"] = inflight
 
     # ---- dominant kernel + launches (live, torch profiler over device-resident steps)
     top_name, top_us, top_per_step, step_us, launches, per = roofline_probe(L, a, b, params)
@@ -508,6 +566,12 @@ def run_ours(args, cfg, world, rank, local):
     roof["share_of_step"] = top_us * top_per_step / step_us if step_us else None
     stages = stage_rooflines(per, 5, cfg, peaks) if per else None
 
+    def _short(nm):
+        return nm.replace("lramm::(anonymous namespace)::", "").replace("void ", "").split("(")[0]
+
+    top_kernels = [{"kernel": _short(nm), "us_per_step": v[0] / 5, "launches_per_step": v[1] // 5}
+                   for nm, v in sorted(per.items(), key=lambda kv: -kv[1][0])[:14]] if per else None
+
     line = {"metric": "effective approx-GEMM TOPS (2mnk/time)", "value": value, "unit": "TOPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
@@ -515,7 +579,7 @@ def run_ours(args, cfg, world, rank, local):
             "data": "synthetic (SURVEY §8(d) spectrum, Haar factors from seeded torch QR)",
             "config": workload_config(cfg, args, world), "clocks": clock_summary, "e2e": e2e,
             "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches, "roofline": roof,
-            "stages": stages, "peaks": peaks.get("live")}
+            "stages": stages, "top_kernels": top_kernels, "peaks": peaks.get("live")}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"], d_ref = cpu_baseline(cfg, a, b)
     else:

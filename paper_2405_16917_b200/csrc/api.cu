@@ -88,7 +88,7 @@ int split_limbs_device(const int32_t *src, int64_t rows, int64_t cols, int64_t l
                        int64_t ldd, cudaStream_t st);
 int lramm_device(const void *, const void *, int, int64_t, int64_t, int64_t, const lramm_params_t &, const double *,
                  const double *, const void *, int, void *, int, int *, void *, size_t, lramm_timings_t *,
-                 cudaStream_t, cudaEvent_t b_ready = nullptr);
+                 cudaStream_t, cudaEvent_t b_ready = nullptr, cudaEvent_t *stage_events = nullptr);
 
 // ---------------------------------------------------------------- host-side device memory
 // One cached device arena + stream for the host-pointer entry points (grow-only,
@@ -98,9 +98,12 @@ struct HostCtx {
   char *buf = nullptr;
   size_t cap = 0;
   cudaStream_t st = nullptr;
-  cudaStream_t copy = nullptr;  // second upload stream (B, Omega_B, C) so A's chain starts first
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  cudaStream_t copy = nullptr;  // upload stream (A, then B, Omega_B, C): A's chain starts first
+  cudaStream_t down = nullptr;  // download stream of lramm_host_lramm (D), behind ev_done
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_done = nullptr;
+  cudaEvent_t ev_t[6] = {};  // stage boundaries of lramm_host_lramm (timing events)
   int *status = nullptr;
+  int *h_status = nullptr;  // pinned copy of the status word (read without another D2H copy)
   int dev = -1;
 };
 // Host entry points lease one context (streams + device buffer) for the duration of a call:
@@ -139,15 +142,23 @@ static int host_reserve(HostCtx &c, size_t bytes) {
     c.cap = 0;
     c.st = nullptr;
     c.copy = nullptr;
-    c.ev_a = c.ev_b = nullptr;
+    c.down = nullptr;
+    c.ev_a = c.ev_b = c.ev_done = nullptr;
+    for (auto &e : c.ev_t) e = nullptr;
     c.status = nullptr;
+    c.h_status = nullptr;
     c.dev = dev;
   }
   if (!c.st) LRAMM_CUDA_TRY(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
   if (!c.copy) LRAMM_CUDA_TRY(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+  if (!c.down) LRAMM_CUDA_TRY(cudaStreamCreateWithFlags(&c.down, cudaStreamNonBlocking));
   if (!c.ev_a) LRAMM_CUDA_TRY(cudaEventCreateWithFlags(&c.ev_a, cudaEventDisableTiming));
   if (!c.ev_b) LRAMM_CUDA_TRY(cudaEventCreateWithFlags(&c.ev_b, cudaEventDisableTiming));
+  if (!c.ev_done) LRAMM_CUDA_TRY(cudaEventCreateWithFlags(&c.ev_done, cudaEventDisableTiming));
+  for (auto &e : c.ev_t)
+    if (!e) LRAMM_CUDA_TRY(cudaEventCreate(&e));
   if (!c.status) LRAMM_CUDA_TRY(cudaMalloc(&c.status, 64));
+  if (!c.h_status) LRAMM_CUDA_TRY(cudaMallocHost(&c.h_status, 64));
   if (bytes > c.cap) {
     if (c.buf) LRAMM_CUDA_TRY(cudaFree(c.buf));
     c.buf = nullptr;
@@ -330,6 +341,13 @@ int lramm_lramm_sharded(const void *a_rows, const void *b_cols, int in_dtype, in
 }
 
 // ---------------------------------------------------------------- host API
+static int status_to_rc(int s) {
+  if (s == LRAMM_ERR_NONCONVERGENCE) return fail(s, "jacobi sweeps did not converge within 60");
+  if (s == LRAMM_ERR_NONFINITE) return fail(s, "cannot quantize non-finite entries");
+  if (s) return fail(s, "device status %d", s);
+  return LRAMM_OK;
+}
+
 static int finish(HostCtx &c) {
   LRAMM_CUDA_TRY(cudaStreamSynchronize(c.st));
   int s = 0;
@@ -484,9 +502,8 @@ int lramm_host_lramm(const void *a, const void *b, int in_dtype, int64_t m, int6
   char *dd = ar.take<char>(m * n * ds);
   char *dc = cmat ? ar.take<char>(m * n * cs) : nullptr;
   void *w = ar.take<char>((int64_t)ws);
-  // uploads overlap the factorisation: A and Omega_A on the compute stream (A's chain starts as
-  // soon as they land), then B, Omega_B (and C) on the copy stream behind them; B's chain
-  // waits only for its own operands (b_ready)
+  // uploads overlap the factorisation: A's chain starts as soon as A (and Omega_A) have landed,
+  // B's chain waits only for its own operands (b_ready); both uploads run on the copy stream
   // Omega may already live on this device (the device generator's cache): used in place
   auto on_device = [&](const void *p) {
     cudaPointerAttributes at;
@@ -497,25 +514,75 @@ int lramm_host_lramm(const void *a, const void *b, int in_dtype, int64_t m, int6
     return at.type == cudaMemoryTypeDevice && at.device == c.dev;
   };
   const double *oa_use = oa, *ob_use = ob;
-  if (on_device(omega_a))
-    oa_use = omega_a;
-  else
-    LRAMM_CUDA_TRY(cudaMemcpyAsync(oa, omega_a, k * wa * 8, cudaMemcpyHostToDevice, c.st));
-  LRAMM_CUDA_TRY(cudaMemcpyAsync(da, a, m * k * es, cudaMemcpyHostToDevice, c.st));
-  LRAMM_CUDA_TRY(cudaEventRecord(c.ev_a, c.st));
-  LRAMM_CUDA_TRY(cudaStreamWaitEvent(c.copy, c.ev_a, 0));
-  if (on_device(omega_b))
-    ob_use = omega_b;
-  else
-    LRAMM_CUDA_TRY(cudaMemcpyAsync(ob, omega_b, n * wb * 8, cudaMemcpyHostToDevice, c.copy));
-  LRAMM_CUDA_TRY(cudaMemcpyAsync(db, b, k * n * es, cudaMemcpyHostToDevice, c.copy));
-  if (cmat) LRAMM_CUDA_TRY(cudaMemcpyAsync(dc, cmat, m * n * cs, cudaMemcpyHostToDevice, c.copy));
-  LRAMM_CUDA_TRY(cudaEventRecord(c.ev_b, c.copy));
-  if (timings) LRAMM_CUDA_TRY(cudaStreamWaitEvent(c.st, c.ev_b, 0));  // stage timings stay comparable
-  LRAMM_TRY(lramm_device(da, db, in_dtype, m, k, n, *params, oa_use, ob_use, dc, c_dtype, dd, d_dtype, c.status, w,
-                         ws, timings, c.st, c.ev_b));
-  LRAMM_CUDA_TRY(cudaMemcpyAsync(d, dd, m * n * ds, cudaMemcpyDeviceToHost, c.st));
-  return finish(c);
+  const bool oa_dev = on_device(omega_a), ob_dev = on_device(omega_b);
+  if (oa_dev) oa_use = omega_a;
+  if (ob_dev) ob_use = omega_b;
+  {
+    // one call's uploads are submitted as a unit (A, then B), all on the copy stream: with several
+    // host threads in flight the copy engine then serves A1 B1 A2 B2 ... instead of A1 A2 .. B1 B2 ..,
+    // so call i's factorisation overlaps call i+1's upload and call i-1's download
+    static std::mutex upload_mu;
+    std::lock_guard<std::mutex> g(upload_mu);
+    if (!oa_dev) LRAMM_CUDA_TRY(cudaMemcpyAsync(oa, omega_a, k * wa * 8, cudaMemcpyHostToDevice, c.copy));
+    LRAMM_CUDA_TRY(cudaMemcpyAsync(da, a, m * k * es, cudaMemcpyHostToDevice, c.copy));
+    LRAMM_CUDA_TRY(cudaEventRecord(c.ev_a, c.copy));
+    if (!ob_dev) LRAMM_CUDA_TRY(cudaMemcpyAsync(ob, omega_b, n * wb * 8, cudaMemcpyHostToDevice, c.copy));
+    LRAMM_CUDA_TRY(cudaMemcpyAsync(db, b, k * n * es, cudaMemcpyHostToDevice, c.copy));
+    if (cmat) LRAMM_CUDA_TRY(cudaMemcpyAsync(dc, cmat, m * n * cs, cudaMemcpyHostToDevice, c.copy));
+    LRAMM_CUDA_TRY(cudaEventRecord(c.ev_b, c.copy));
+  }
+  LRAMM_CUDA_TRY(cudaStreamWaitEvent(c.st, c.ev_a, 0));
+  // (the rsvd stage time of a host call therefore includes the tail of B's upload)
+  // Device-side FIFO of concurrent host calls: kernels of a large product fill the GPU, so calls
+  // whose factorisations interleave all finish late and their downloads queue up behind one
+  // another (measured at c3, three calls in flight: first download at 38 ms instead of 19 ms).
+  // Each large call therefore waits, on the device, for the call before it in its slot; copies
+  // are not gated, so call i+1 uploads and call i-1 downloads while call i computes.  Small
+  // products (latency-bound, e.g. the batched 2048^3 pairs) keep running side by side.
+  static const int slots_env = [] {
+    const char *e = getenv("LRAMM_HOST_COMPUTE_SLOTS");
+    return e ? atoi(e) : -1;
+  }();
+  const bool big = std::max(std::max(m, n), k) >= 4096;
+  const int slots = slots_env >= 0 ? std::min(slots_env, 8) : (big ? 1 : 0);
+  {
+    static std::mutex gate_mu;
+    static cudaEvent_t last_done[8][64] = {};  // [slot][device]
+    static unsigned long long ticket = 0;
+    std::unique_lock<std::mutex> g(gate_mu, std::defer_lock);
+    int slot = 0;
+    const int dv = c.dev & 63;
+    if (slots > 0) {
+      g.lock();
+      slot = (int)(ticket++ % (unsigned)slots);
+      if (last_done[slot][dv]) LRAMM_CUDA_TRY(cudaStreamWaitEvent(c.st, last_done[slot][dv], 0));
+    }
+    LRAMM_TRY(lramm_device(da, db, in_dtype, m, k, n, *params, oa_use, ob_use, dc, c_dtype, dd, d_dtype, c.status, w,
+                           ws, timings, c.st, c.ev_b, timings ? c.ev_t : nullptr));
+    LRAMM_CUDA_TRY(cudaEventRecord(c.ev_done, c.st));
+    if (slots > 0) last_done[slot][dv] = c.ev_done;
+  }
+  // D goes down on its own stream behind ev_done: the compute stream ends with the event the next
+  // call in the FIFO waits for (with the copy queued on the compute stream itself the next call's
+  // kernels started only when the download had finished: scripts/e2e_timeline.py)
+  // The status word travels on the same stream just before D, into pinned memory: a separate
+  // synchronous read after the download would queue behind the other calls' pending downloads in
+  // the copy engine's FIFO (measured: four calls in flight all returned together).
+  LRAMM_CUDA_TRY(cudaStreamWaitEvent(c.down, c.ev_done, 0));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(c.h_status, c.status, sizeof(int), cudaMemcpyDeviceToHost, c.down));
+  LRAMM_CUDA_TRY(cudaMemcpyAsync(d, dd, m * n * ds, cudaMemcpyDeviceToHost, c.down));
+  LRAMM_CUDA_TRY(cudaStreamSynchronize(c.down));
+  const int rc = status_to_rc(*c.h_status);
+  if (timings && rc == LRAMM_OK) {
+    float t[5];
+    for (int i = 0; i < 5; ++i) LRAMM_CUDA_TRY(cudaEventElapsedTime(&t[i], c.ev_t[i], c.ev_t[i + 1]));
+    timings->rsvd_ms = t[0];
+    timings->scaling_ms = t[1];
+    timings->gemm1_ms = t[2];
+    timings->gemm2_ms = t[3];
+    timings->gemm3_ms = t[4];
+  }
+  return rc;
 }
 
 }  // extern "C"

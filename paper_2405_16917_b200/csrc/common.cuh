@@ -10,9 +10,24 @@
 #include <mutex>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3 (resolved lazily; a no-op without an attached tool)
+
 #include "../../include/lramm_cuda.h"
 
 namespace lramm {
+
+// NVTX range over the host-side issue of one pipeline stage (the reference's stage names,
+// pipeline.py:40: rsvd / scaling / gemm1 / gemm2 / gemm3); nsys / ncu attribute the kernels
+// launched inside it
+struct NvtxStages {
+  bool open = false;
+  void next(const char *name) {  // closes the running stage, opens `name` (nullptr: just close)
+    if (open) nvtxRangePop();
+    open = name != nullptr;
+    if (open) nvtxRangePushA(name);
+  }
+  ~NvtxStages() { next(nullptr); }  // error returns leave no range open
+};
 
 // ------------------------------------------------------------------ status
 void set_error(const char *fmt, ...);

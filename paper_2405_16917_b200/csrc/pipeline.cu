@@ -463,6 +463,8 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
     if (rc) LRAMM_TRY(qr_report_breakdown_device(b.qr_ws, b.qr_bytes, m, w, b.compl_st, st));
     return LRAMM_OK;
   };
+  NvtxStages nv;
+  nv.next("rsvd.sketch");
   if (b.fast) {
     // Y = X . Omega at sketch_bits
     if (pair)
@@ -489,6 +491,7 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
   if (b.fast && P.power_iters > 0) LRAMM_TRY(join_helper());
   for (int it = 0; it < P.power_iters; ++it) {
     // Z = X^T Q ; Qz = qr(Z) ; Y = X Qz ; Q = qr(Y)   (rsvd.py:60-64)
+    nv.next("rsvd.power");
     if (b.fast) {
       LRAMM_TRY(quant(b.Q, LRAMM_F64, rows, w, w, P.power_bits, gran_r, 1, b.qq, nullptr, b.qz_ws, b.qz_bytes, st,
                       nullptr, s_rows));
@@ -510,6 +513,7 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
     LRAMM_TRY(qr(b.Y, rows, b.Q, qr_rows, b.gram));
   }
   // Bs^T = X^T Q   (rsvd.py:77, evaluated transposed)
+  nv.next("rsvd.project");
   if (b.fast) {
     LRAMM_TRY(join_helper());
     LRAMM_TRY(quant(b.Q, LRAMM_F64, rows, w, w, P.proj_bits, gran_r, 1, b.qq, nullptr, b.qz_ws, b.qz_bytes, st, nullptr,
@@ -520,10 +524,12 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
     if (red_rows) LRAMM_TRY(red_rows->sum_f64(b.BsT, (size_t)(cols * w), st));
   }
   // SVD(Bs): u = H, v = Bs^T H diag(s)^-1   (rsvd.py:78, _jacobi.py)
+  nv.next("rsvd.small_svd");
   LRAMM_TRY(svd_tall_device(b.BsT, cols, w, w, nullptr, w, b.s, b.H, w, b.info, b.compl_st, b.svd_ws, b.svd_bytes,
                              st, qr_cols));
   // v = Bs^T H diag(s)^-1 on the helper stream, concurrent with the lift U = Q u (rsvd.py:79-81);
   // both then truncated to r (rsvd.py:84-94)
+  nv.next("rsvd.lift");
   HelperStream &hv = helper_stream(st);
   LRAMM_CUDA_TRY(cudaEventRecord(hv.fork, st));
   LRAMM_CUDA_TRY(cudaStreamWaitEvent(hv.st, hv.fork, 0));
@@ -677,7 +683,7 @@ size_t lramm_ws_bytes(int64_t m, int64_t k, int64_t n, const lramm_params_t &P, 
 int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t k, int64_t n, const lramm_params_t &P,
                  const double *omega_a, const double *omega_b, const void *c, int c_dtype, void *d, int d_dtype,
                  int *status, void *ws, size_t ws_bytes, lramm_timings_t *timings, cudaStream_t st,
-                 cudaEvent_t b_ready) {
+                 cudaEvent_t b_ready, cudaEvent_t *stage_events) {
   LRAMM_TRY(validate_params(P, true));
   if (P.rank < 2) return fail(LRAMM_ERR_PARAM, "rank must be >= 2, got %d", P.rank);
   if (in_dtype != LRAMM_F32 && in_dtype != LRAMM_F64) return fail(LRAMM_ERR_PARAM, "inputs must be F32 or F64");
@@ -701,11 +707,20 @@ int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t 
   LrammBufs L = carve_lramm(ar, m, k, n, in_dtype, P);
   if (!ar.ok()) return fail(LRAMM_ERR_WORKSPACE, "lramm: workspace too small (%zu needed)", ar.off);
 
+  // stage_events (6 caller-owned timing events): the stage boundaries are recorded into them and
+  // the caller reads the times after its own synchronisation (the host entry point enqueues the
+  // download of D first); otherwise timings != NULL synchronises here
   cudaEvent_t ev[6] = {};
-  if (timings)
+  if (stage_events)
+    for (int i = 0; i < 6; ++i) ev[i] = stage_events[i];
+  else if (timings)
     for (int i = 0; i < 6; ++i) LRAMM_CUDA_TRY(cudaEventCreate(&ev[i]));
+  NvtxStages nv;
+  static const char *const kStage[6] = {"lramm.rsvd", "lramm.scaling", "lramm.gemm1", "lramm.gemm2", "lramm.gemm3",
+                                        nullptr};
   auto mark = [&](int i) -> int {
-    if (timings) LRAMM_CUDA_TRY(cudaEventRecord(ev[i], st));
+    nv.next(kStage[i]);
+    if (timings || stage_events) LRAMM_CUDA_TRY(cudaEventRecord(ev[i], st));
     return LRAMM_OK;
   };
   LRAMM_TRY(mark(0));
@@ -766,7 +781,7 @@ int lramm_device(const void *a, const void *b, int in_dtype, int64_t m, int64_t 
   LRAMM_LAUNCH_CHECK();
   summarize_status_kernel<<<1, 32, 0, st>>>(L.jinfo, 4, L.nonfinite, nullptr, status);
   LRAMM_LAUNCH_CHECK();
-  if (timings) {
+  if (timings && !stage_events) {
     LRAMM_CUDA_TRY(cudaEventSynchronize(ev[5]));
     float t[5];
     for (int i = 0; i < 5; ++i) LRAMM_CUDA_TRY(cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]));
