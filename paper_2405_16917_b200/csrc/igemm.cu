@@ -123,7 +123,7 @@ constexpr int kSmemBudget = 200 * 1024;
 enum { EK_I32 = 0, EK_I32_ATOMIC = 1, EK_F32 = 2, EK_F64 = 3, EK_I64_ADD = 4 };
 
 template <int EK, bool TRANS, bool AB>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)  // two CTAs per SM in the shallow-ring mode: registers stay <= 96
     igemm_tn_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                     int64_t M, int64_t N, int64_t K, int BN, int stages, int kb_per_split, EpiDev epi) {
   extern __shared__ uint8_t smem_raw[];
