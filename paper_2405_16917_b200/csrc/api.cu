@@ -557,8 +557,13 @@ int lramm_host_lramm(const void *a, const void *b, int in_dtype, int64_t m, int6
       slot = (int)(ticket++ % (unsigned)slots);
       if (last_done[slot][dv]) LRAMM_CUDA_TRY(cudaStreamWaitEvent(c.st, last_done[slot][dv], 0));
     }
-    LRAMM_TRY(lramm_device(da, db, in_dtype, m, k, n, *params, oa_use, ob_use, dc, c_dtype, dd, d_dtype, c.status, w,
-                           ws, timings, c.st, c.ev_b, timings ? c.ev_t : nullptr));
+    const int rc_dev = lramm_device(da, db, in_dtype, m, k, n, *params, oa_use, ob_use, dc, c_dtype, dd, d_dtype,
+                                    c.status, w, ws, timings, c.st, c.ev_b, timings ? c.ev_t : nullptr);
+    if (rc_dev != LRAMM_OK) {  // refused before or while issuing: the uploads still read the caller's buffers
+      cudaStreamSynchronize(c.copy);
+      cudaStreamSynchronize(c.st);
+      return rc_dev;
+    }
     LRAMM_CUDA_TRY(cudaEventRecord(c.ev_done, c.st));
     if (slots > 0) last_done[slot][dv] = c.ev_done;
   }
