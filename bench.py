@@ -752,8 +752,9 @@ def run_sharded(args, cfg, world, rank, local):
 
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full` captures
 # (profiles/r01_ncu_jacobi_c2.txt)
-NCU_DRAM_BYTES = {
-    "jacobi_cluster_kernel<9, false>": 639488,
+NCU_DRAM_BYTES = {  # dram__bytes_read.sum + dram__bytes_write.sum of one launch, ncu --set full
+    "jacobi_cluster_kernel<9, false>": 639488,  # profiles/r01_ncu_jacobi_c2.txt
+    "sytrd_push_kernel<17, 0>": 2426624,        # profiles/r02_ncu_sytrd_c3.txt (the one load of the Gram matrix)
 }
 
 
@@ -797,9 +798,10 @@ def dominant_roofline(name, us, cfg, peaks):
         # small SVD): 4/3 w^3 flops in w - 2 dependent steps
         flops = 4.0 / 3.0 * w ** 3
         achieved = flops / (us * 1e-6) / 1e12
+        traffic = next((v for k, v in NCU_DRAM_BYTES.items() if k in name), None)
         return {"bound": "tensor", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak, "traffic": None, "algorithmic_flops": flops,
-                "peak_source": FP64_PEAK_SOURCE,
+                "frac": achieved / fp64_peak, "traffic": traffic, "algorithmic_flops": flops,
+                "peak_source": FP64_PEAK_SOURCE, "class": "latency-bound (CUDA-core fp64, not a throughput kernel)",
                 "note": "latency-bound: w - 2 dependent reflector steps, each one DSMEM exchange (st.async + "
                         "mbarrier) across the cluster; the matrix stays in registers / shared memory (no DRAM "
                         "traffic beyond the one load of the Gram matrix)"}
