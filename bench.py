@@ -673,18 +673,20 @@ def run_sharded(args, cfg, world, rank, local):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    t_end = time.time() + 1.0
-    while time.time() < t_end:  # keep the GPU loaded for the clock sampler (untimed)
-        graph.replay()
-        torch.cuda.synchronize()
-    clocks.__exit__(None, None, None)
-    clock_summary = clocks.summary(clk_mark)
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-        torch.distributed.barrier()
     ms_per_step = ms / args.steps
+    # keep the GPU loaded for the clock sampler (untimed): the SAME number of replays on every rank
+    # (each replay contains collectives), derived from the all-reduced step time
+    for _ in range(int(min(500, max(1, 1000.0 / max(ms_per_step, 1e-3))))):
+        graph.replay()
+    torch.cuda.synchronize()
+    clocks.__exit__(None, None, None)
+    clock_summary = clocks.summary(clk_mark)
+    if world > 1:
+        torch.distributed.barrier()
     value = effective_ops(cfg) / (ms_per_step * 1e-3) / 1e12
 
     # e2e: this rank's shards from pinned host memory, its fp64 D rows back to the host, every step

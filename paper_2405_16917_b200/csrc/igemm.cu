@@ -214,6 +214,16 @@ __global__ void __launch_bounds__(kThreads, 2)  // two CTAs per SM in the shallo
     const int etid = threadIdx.x - 64;     // 0..255
     const int rloc = quarter * 32 + lane;
     const int64_t row = m0 + rloc;
+    // per-column scales of this tile -> shared memory while the mainloop runs (the epilogue read
+    // them from global memory per element: long-scoreboard stalls of 14 warps per issue at the c3
+    // sketch shape, profiles/r02_ncu_igemm_c3.txt)
+    __shared__ double cs_sh[256];
+    constexpr bool RAW0 = EK == EK_I32 || EK == EK_I32_ATOMIC || EK == EK_I64_ADD;
+    if (!RAW0 && epi.col_scale != nullptr && epi.col_scale_inc != 0) {
+      for (int cidx = etid; cidx < BN; cidx += 256)
+        cs_sh[cidx] = epi.col_scale[min(n0 + cidx, N - 1) * epi.col_scale_inc];
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
     if (a4) {
       // mainloop role of the epilogue warps: unpack each stage's packed A tile (BM rows x 64 B of
       // nibbles) into the int8 tile the MMA reads, in the TMA SWIZZLE_128B layout (16-byte chunk c
@@ -284,8 +294,7 @@ __global__ void __launch_bounds__(kThreads, 2)  // two CTAs per SM in the shallo
           if (tensor_scale) {
             v[j] = div_exact((double)(int32_t)r[j], s_t, y_t);
           } else {
-            const int64_t col = min(col0 + j, N - 1);
-            const double sc = __dmul_rn(rs, epi.col_scale[col * epi.col_scale_inc]);
+            const double sc = __dmul_rn(rs, cs_sh[cb + j]);
             v[j] = div_exact((double)(int32_t)r[j], sc, __drcp_rn(sc));
           }
           if constexpr (AB) v[j] = epi_alpha_beta(epi, v[j], row, min(col0 + j, N - 1));
@@ -334,8 +343,7 @@ __global__ void __launch_bounds__(kThreads, 2)  // two CTAs per SM in the shallo
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const int64_t col = min(n0 + cb + j, N - 1);
-          const double s = __dmul_rn(rs, epi.col_scale[col * epi.col_scale_inc]);
+          const double s = __dmul_rn(rs, cs_sh[min(cb + j, BN - 1)]);
           tile[rloc * 33 + half * 16 + j] = div_exact((double)(int32_t)r[j], s, __drcp_rn(s));
         }
       }
@@ -600,7 +608,7 @@ int igemm_device(int64_t M, int64_t N, int64_t K, const int8_t *a, int64_t lda, 
   // so one CTA's epilogue overlaps the other's loads and MMAs (c5 E3 131072x8192x1024: 4.1 ->
   // 2.7 ms; c3 E3: 239 -> 143 us); single-wave grids keep the deep ring
   const int64_t ctas = ceil_div(M, BM) * ceil_div(N, BN) * split_k;
-  const int two_per_sm = (113 * 1024 - 2048) / stage_bytes;
+  const int two_per_sm = (109 * 1024) / stage_bytes;  // + barriers, alignment slack and 2 KB static (cs_sh) <= 113 KB
   if (ctas > num_sms() && two_per_sm >= 2) stages = std::min(stages, two_per_sm);
   const int smem = stages * stage_bytes + (3 * stages + 2) * 8 + 1024 + 64;
   CUtensorMap ta, tb;
