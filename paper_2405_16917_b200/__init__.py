@@ -10,7 +10,14 @@ dataclasses and the error types, computed by hand-written sm_100a CUDA
 generators on the host in `matio.py`).
 """
 
-from . import _native  # noqa: F401  (fails loudly if liblramm_cuda.so is missing)
+import os as _os
+
+# Every product runs on several streams (two rsvd chains, helper and copy streams) and concurrent
+# products multiply that; the default 8 hardware work queues make unrelated streams share a queue
+# and serialise.  Only effective when set before the process creates its CUDA context.
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+from . import _native  # noqa: E402,F401  (fails loudly if liblramm_cuda.so is missing)
 from .errors import (
     DegenerateDenominatorError,
     FormatError,
