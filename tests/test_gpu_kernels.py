@@ -339,6 +339,25 @@ def test_qr_orthonormal_and_spans(mw):
     assert np.max(np.abs(q * sign - qh)) <= 1e-10
 
 
+@pytest.mark.parametrize("mw", [(2400, 544), (2200, 520), (2304, 576), (4400, 1056), (9000, 272), (4500, 1040)])
+def test_qr_explicit_inverse_path(mw):
+    """Tall sketches (w >= 512 with m >= 4 w, or w >= 256 with m >= 32 w) take Q = Y L^-T as the
+    tile-doubling triangular inverse + one DMMA GEMM (factor.cu trinv_tiles_kernel): full and
+    partial last tiles, odd tile counts, and the widest sketch (33 tiles)."""
+    from paper_2405_16917_b200.rsvd import _qr_device
+
+    m, w = mw
+    y = O.synth(m, w, "exp:40", 7, 0, 0).astype(np.float64) @ np.diag(np.linspace(1, 3, w))
+    q = _qr_device(torch.from_numpy(y).to(dev())).cpu().numpy()
+    assert np.all(np.isfinite(q))
+    assert np.linalg.norm(q.T @ q - np.eye(w)) <= 1e-12 * np.sqrt(w)
+    qh = np.linalg.qr(y)[0]
+    sign = np.sign(np.sum(q * qh, axis=0))
+    assert np.max(np.abs(q * sign - qh)) <= 1e-10
+    q2 = _qr_device(torch.from_numpy(y).to(dev())).cpu().numpy()
+    assert np.array_equal(q, q2)  # deterministic
+
+
 def test_qr_rank_deficient_falls_back_to_householder():
     from paper_2405_16917_b200.rsvd import _qr_device
 
