@@ -85,6 +85,23 @@ def test_shape_errors_raise_before_device():
         L.lramm(a, a, L.LrammParams(rank=2, bits=(25, 8, 8)))
 
 
+def test_oracle_svd_size_cap_is_the_references():
+    """matcore.py:23, :240-243 and test_matcore.py:241: min dim > 512 raises OracleLimitError before
+    any device work; the cap is a module constant read at call time, so a harness can raise it
+     -- without a GPU the raised cap then reaches the no-fallback error instead."""
+    import sys
+
+    import paper_2405_16917_b200 as L
+
+    rsvd = sys.modules["paper_2405_16917_b200.rsvd"]  # the package re-exports the rsvd function under this name
+    assert rsvd.ORACLE_MAX_MIN_DIM == 512
+    with pytest.raises(L.OracleLimitError):
+        L.oracle_svd(np.zeros((513, 600)))
+    with pytest.raises(L.OracleLimitError):
+        L.oracle_svd(np.zeros((4096, 544)))
+    assert issubclass(L.OracleLimitError, ValueError)  # errors.py:16 hierarchy
+
+
 def test_no_cpu_fallback_without_device():
     import torch
 
