@@ -66,7 +66,7 @@ int qr_device(const double *, int64_t, int64_t, int64_t, double *, int64_t, doub
               const Coll *rows_coll = nullptr);
 size_t qr_ws_bytes(int64_t, int64_t);
 int svd_tall_device(const double *, int64_t, int64_t, int64_t, double *, int64_t, double *, double *, int64_t, int *,
-                    int *, void *, size_t, cudaStream_t, const Coll *rows_coll = nullptr);
+                    int *, void *, size_t, cudaStream_t, const Coll *rows_coll = nullptr, bool fast = false);
 size_t svd_tall_ws_bytes(int64_t, int64_t);
 int transpose_device(const double *, int64_t, int64_t, int64_t, double *, int64_t, cudaStream_t);
 size_t rsvd_ws_bytes(int64_t, int64_t, const lramm_params_t &, int);

@@ -49,7 +49,7 @@ int svd_tall_pside_device(const double *T, int64_t m, int64_t n, int64_t ldt, co
                           cudaStream_t st);
 int svd_tall_device(const double *T, int64_t m, int64_t n, int64_t ldt, double *pside, int64_t ldp, double *s,
                     double *h, int64_t ldh, int *info, int *status, void *ws, size_t ws_bytes, cudaStream_t st,
-                    const Coll *rows_coll = nullptr);
+                    const Coll *rows_coll = nullptr, bool fast = false);
 size_t svd_tall_ws_bytes(int64_t m, int64_t n);
 int qr_report_breakdown_device(void *ws, size_t ws_bytes, int64_t m, int64_t w, int *status, cudaStream_t st);
 
@@ -526,7 +526,7 @@ int run_rsvd(const void *x, int x_dtype, RsvdBufs &b, const lramm_params_t &P, c
   // SVD(Bs): u = H, v = Bs^T H diag(s)^-1   (rsvd.py:78, _jacobi.py)
   nv.next("rsvd.small_svd");
   LRAMM_TRY(svd_tall_device(b.BsT, cols, w, w, nullptr, w, b.s, b.H, w, b.info, b.compl_st, b.svd_ws, b.svd_bytes,
-                             st, qr_cols));
+                             st, qr_cols, b.fast));
   // v = Bs^T H diag(s)^-1 on the helper stream, concurrent with the lift U = Q u (rsvd.py:79-81);
   // both then truncated to r (rsvd.py:84-94)
   nv.next("rsvd.lift");
