@@ -7,6 +7,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <map>
 #include <mutex>
 #include <string>
 
@@ -96,6 +97,87 @@ struct PerDeviceOnce {
     if (dev < 0 || dev >= kMaxDev) return f();
     std::call_once(flags[dev], [&] { err[dev] = f(); });
     return err[dev];
+  }
+};
+
+// ------------------------------------------------------------------ conditional graph sections
+// The rarely taken branches of the factorisations (second CholeskyQR pass, Cholesky path of the
+// closed-form update) are sequences of ~10 kernels that each read a device flag and return at
+// once: cheap as work, but every one is a graph node (~1-2.5 us of launch chain; c4 is bound by
+// its node count).  While the caller's stream is being captured into a CUDA graph the sequence
+// is recorded instead into the body of an IF node (CUDA 12.4 conditional nodes): a one-thread
+// kernel sets the node's condition from the flag, the body is captured on an auxiliary stream
+// into the node's body graph, and the caller's capture continues behind the node.  Outside a
+// capture (eager launches, the host entry points) nothing changes: stream() is the caller's
+// stream and the kernels gate themselves as before (they keep their gates inside the body too).
+static __global__ void cond_set_kernel(cudaGraphConditionalHandle h, const int *flag, int run_if_nonzero) {
+  cudaGraphSetConditional(h, ((*flag != 0) == (run_if_nonzero != 0)) ? 1u : 0u);
+}
+
+struct CondIf {
+  cudaStream_t outer = nullptr, body = nullptr;
+  cudaGraphNode_t node = nullptr;
+  bool active = false;
+  static bool enabled() {
+    static const bool on = [] {
+      const char *e = getenv("LRAMM_GRAPH_COND");
+      return !e || atoi(e) != 0;
+    }();
+    return on;
+  }
+  static cudaStream_t aux_stream(cudaStream_t main) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, cudaStream_t> table;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    cudaStream_t &x = table[{dev, main}];
+    if (!x) cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+    return x;
+  }
+  int begin(cudaStream_t st, const int *flag, bool run_if_nonzero) {
+    outer = st;
+    if (!enabled()) return LRAMM_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    if (cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd) != cudaSuccess || cs != cudaStreamCaptureStatusActive) {
+      cudaGetLastError();
+      return LRAMM_OK;  // not capturing: the kernels gate themselves
+    }
+    cudaGraphConditionalHandle h;
+    LRAMM_CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+    cond_set_kernel<<<1, 1, 0, st>>>(h, flag, run_if_nonzero ? 1 : 0);
+    LRAMM_LAUNCH_CHECK();
+    LRAMM_CUDA_TRY(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeIf;
+    p.conditional.size = 1;
+    LRAMM_CUDA_TRY(cudaGraphAddNode(&node, g, deps, nd, &p));
+    body = aux_stream(st);
+    LRAMM_CUDA_TRY(cudaStreamBeginCaptureToGraph(body, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                 cudaStreamCaptureModeRelaxed));
+    active = true;
+    return LRAMM_OK;
+  }
+  cudaStream_t stream() const { return active ? body : outer; }
+  int end() {
+    if (!active) return LRAMM_OK;
+    active = false;
+    cudaGraph_t out = nullptr;
+    LRAMM_CUDA_TRY(cudaStreamEndCapture(body, &out));
+    LRAMM_CUDA_TRY(cudaStreamUpdateCaptureDependencies(outer, &node, 1, cudaStreamSetCaptureDependencies));
+    return LRAMM_OK;
+  }
+  ~CondIf() {
+    if (active) {  // error return inside the section: close the body capture
+      cudaGraph_t out = nullptr;
+      cudaStreamEndCapture(body, &out);
+      cudaStreamUpdateCaptureDependencies(outer, &node, 1, cudaStreamSetCaptureDependencies);
+    }
   }
 };
 

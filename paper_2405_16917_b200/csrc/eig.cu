@@ -1133,11 +1133,18 @@ int eig_precondition_device(double *R, int n, int *jac_gate, void *ws, size_t ws
   LRAMM_TRY(dgemm_device_ex(1, n, n, n, w.P, n, w.P, n, w.S, n, w.gemm, w.gemm_bytes, st, sym));
   offrel_check_kernel<<<dim3(eblocks, batch), 256, 0, st>>>(w.S, n, (int64_t)n * n, 1e-26, w.flags, 2, -1);
   LRAMM_LAUNCH_CHECK();
-  refine_e_kernel<<<dim3(eblocks, batch), 256, 0, st>>>(w.S, n, (int64_t)n * n, 1e-4, w.E, w.flags);
-  LRAMM_LAUNCH_CHECK();
-  refine_gate_kernel<<<dim3(eblocks, batch), 256, 0, st>>>(w.E, n, (int64_t)n * n, w.flags);
+  // P2 = P when the first check passed; otherwise the refinement below (mutually exclusive writers of
+  // P2).  The refinement and its second check are one IF node of a captured graph (batch == 1).
+  copy_if_converged_kernel<<<dim3(eblocks, batch), 256, 0, st>>>(w.P, w.P2, (int64_t)n * n, (int64_t)n * n, w.flags);
   LRAMM_LAUNCH_CHECK();
   {
+    CondIf sec;
+    if (batch == 1) LRAMM_TRY(sec.begin(st, w.flags + 2, true));
+    cudaStream_t s2 = sec.stream();
+    refine_e_kernel<<<dim3(eblocks, batch), 256, 0, s2>>>(w.S, n, (int64_t)n * n, 1e-4, w.E, w.flags);
+    LRAMM_LAUNCH_CHECK();
+    refine_gate_kernel<<<dim3(eblocks, batch), 256, 0, s2>>>(w.E, n, (int64_t)n * n, w.flags);
+    LRAMM_LAUNCH_CHECK();
     DgemmOptions f;  // F = E + E E / 2   (into D: free after the Lowdin step)
     f.alpha = 0.5;
     f.beta = 1.0;
@@ -1145,7 +1152,7 @@ int eig_precondition_device(double *R, int n, int *jac_gate, void *ws, size_t ws
     f.ldci = n;
     f.gate = w.flags + 2;
     f.gate_run_if_nonzero = 1;
-    LRAMM_TRY(dgemm_device_ex(0, n, n, n, w.E, n, w.E, n, w.D, n, w.gemm, w.gemm_bytes, st, f));
+    LRAMM_TRY(dgemm_device_ex(0, n, n, n, w.E, n, w.E, n, w.D, n, w.gemm, w.gemm_bytes, s2, f));
     DgemmOptions rf;  // P2 = P + P F
     rf.alpha = 1.0;
     rf.beta = 1.0;
@@ -1153,16 +1160,15 @@ int eig_precondition_device(double *R, int n, int *jac_gate, void *ws, size_t ws
     rf.ldci = n;
     rf.gate = w.flags + 2;
     rf.gate_run_if_nonzero = 1;
-    LRAMM_TRY(dgemm_device_ex(0, n, n, n, w.P, n, w.D, n, w.P2, n, w.gemm, w.gemm_bytes, st, rf));
-    copy_if_converged_kernel<<<dim3(eblocks, batch), 256, 0, st>>>(w.P, w.P2, (int64_t)n * n, (int64_t)n * n, w.flags);
+    LRAMM_TRY(dgemm_device_ex(0, n, n, n, w.P, n, w.D, n, w.P2, n, w.gemm, w.gemm_bytes, s2, rf));
+    DgemmOptions sg = sym;
+    sg.gate = w.flags + 2;
+    sg.gate_run_if_nonzero = 1;
+    LRAMM_TRY(dgemm_device_ex(1, n, n, n, w.P2, n, w.P2, n, w.S, n, w.gemm, w.gemm_bytes, s2, sg));
+    offrel_check_kernel<<<dim3(eblocks, batch), 256, 0, s2>>>(w.S, n, (int64_t)n * n, 1e-26, w.flags, 3, 2);
     LRAMM_LAUNCH_CHECK();
-    DgemmOptions s2 = sym;
-    s2.gate = w.flags + 2;
-    s2.gate_run_if_nonzero = 1;
-    LRAMM_TRY(dgemm_device_ex(1, n, n, n, w.P2, n, w.P2, n, w.S, n, w.gemm, w.gemm_bytes, st, s2));
+    LRAMM_TRY(sec.end());
   }
-  offrel_check_kernel<<<dim3(eblocks, batch), 256, 0, st>>>(w.S, n, (int64_t)n * n, 1e-26, w.flags, 3, 2);
-  LRAMM_LAUNCH_CHECK();
   // R' = P2^T (the Jacobi operand, column-major W')
   LRAMM_TRY(transpose_device(w.P2, n, n, n, R, n, st));
   jacobi_gate_kernel<<<1, 32, 0, st>>>(w.flags, jac_gate, batch);
