@@ -785,12 +785,16 @@ __global__ void __launch_bounds__(256) backtransform_kernel(const double *__rest
       for (int c = rc; c < nb; ++c) acc = fma(ts[rc][c], w1[c][sc], acc);
       w2[rc][sc] = acc;
     }
-    // Z[j][s] -= sum_c v_{k0+c}[j] W2[c][s]
+    // Z[j][s] -= sum_c v_{k0+c}[j] W2[c][s]   (a block whose vectors fit one chunk is still staged
+    // from the W1 pass: half the L2 traffic of the kernel at w <= 657)
+    const bool single = k0 + 1 + jchunk >= n;
     for (int j0 = k0 + 1; j0 < n; j0 += jchunk) {
       const int len = min(jchunk, n - j0);
       __syncthreads();
-      stage(k0, nb, j0, len);
-      __syncthreads();
+      if (!single) {
+        stage(k0, nb, j0, len);
+        __syncthreads();
+      }
       double w2r[kNB];
 #pragma unroll
       for (int c = 0; c < kNB; ++c) w2r[c] = w2[c][sc];  // zero beyond nb (T_b is)
