@@ -147,7 +147,10 @@ struct CondIf {
       return LRAMM_OK;  // not capturing: the kernels gate themselves
     }
     cudaGraphConditionalHandle h;
-    LRAMM_CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+    if (cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault) != cudaSuccess) {
+      cudaGetLastError();  // a driver without conditional nodes: the kernels gate themselves
+      return LRAMM_OK;
+    }
     cond_set_kernel<<<1, 1, 0, st>>>(h, flag, run_if_nonzero ? 1 : 0);
     LRAMM_LAUNCH_CHECK();
     LRAMM_CUDA_TRY(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
