@@ -69,6 +69,21 @@ __device__ __forceinline__ double div_exact(double a, double s, double y) {
   return q1;
 }
 
+// a / s for an output that is rounded to fp32 next (and used for nothing else): a double whose
+// fp32 rounding equals that of the correctly rounded fp64 quotient.  q0 = RN(a y), y = RN(1/s), lies
+// within 2.5 ulp64 of RN(a / s); the two round to the same float unless q0 sits within a few ulp64
+// of a midpoint between adjacent floats (the 29 mantissa bits below fp32 precision near 2^28) or
+// outside the normal fp32 range -- only then the exact division runs (~2^-24 of the elements).
+// The fp32-output epilogue is fp64-pipe bound otherwise: 15 fp64 instructions per element.
+__device__ __forceinline__ double div_for_f32(double a, double s, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const long long b = __double_as_longlong(q0);
+  const int ex = (int)((b >> 52) & 0x7FF);
+  const unsigned lo = (unsigned)b & 0x1FFFFFFFu;
+  if (ex >= 1023 - 120 && ex <= 1023 + 120 && (lo - 0x0FFFFFF8u) > 16u) return q0;
+  return div_exact(a, s, y);
+}
+
 // reference dequantisation + alpha/beta on one accumulator (bit-exact IEEE fp64)
 template <typename AccT>
 __device__ __forceinline__ double epi_value(const EpiDev &e, AccT acc, int64_t row, int64_t col) {
@@ -292,7 +307,10 @@ __global__ void __launch_bounds__(kThreads, 2)  // two CTAs per SM in the shallo
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           if (tensor_scale) {
-            v[j] = div_exact((double)(int32_t)r[j], s_t, y_t);
+            if constexpr (EK == EK_F32 && !AB)
+              v[j] = div_for_f32((double)(int32_t)r[j], s_t, y_t);
+            else
+              v[j] = div_exact((double)(int32_t)r[j], s_t, y_t);
           } else {
             const double sc = __dmul_rn(rs, cs_sh[cb + j]);
             v[j] = div_exact((double)(int32_t)r[j], sc, __drcp_rn(sc));
